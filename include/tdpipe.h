@@ -1,0 +1,211 @@
+/*
+ * tdpipe.h -- C ABI of the B200-native TD-Pipe hot path.
+ *
+ * TD-Pipe (arxiv 2506.10470): temporally-disaggregated pipeline-parallel LLM
+ * inference.  The library owns a Llama-style model sharded by layer over
+ * pipeline stages (§2.2.3 "PP splits a model layer-wise"),
+ * a paged KV cache per stage, and the hierarchy controller (PAPER.md:295-314
+ * §3.2) that alternates long prefill phases and long decode phases using
+ * Alg.1, inter-batch work stealing and
+ * the spatial-temporal intensity switch (Eq.1/Eq.2).
+ *
+ * Conventions
+ *  - Every call returns td_status (0 = TD_OK, < 0 = error); no C++ exception
+ *    crosses the ABI.  On error, td_last_error(ctx) holds a message.
+ *  - All pointers in signatures are HOST pointers unless stated otherwise;
+ *    the library copies what it needs (caller keeps ownership).
+ *  - A td_ctx must not be used by two caller threads at once.
+ *  - Token ids are int32; activations crossing the ABI are fp32 row-major.
+ *  - Device memory, streams, kernels and NCCL communicators are owned by the
+ *    ctx and released by td_destroy.
+ */
+#ifndef TDPIPE_H_
+#define TDPIPE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t td_status;
+#define TD_OK 0
+#define TD_EINVAL (-1)   /* bad argument / shape (e.g. n_stages > n_layers) */
+#define TD_ENOMEM (-2)   /* weights or KV pool do not fit in HBM          */
+#define TD_ECUDA (-3)    /* CUDA runtime / driver error, or no sm_100 device             */
+#define TD_ENCCL (-4)    /* NCCL error (multi-process pipeline)                          */
+#define TD_ERANGE (-5)   /* request too long for max_seq_len / KV pool; buffer too small */
+#define TD_ESTATE (-6)   /* call not valid in the current state                          */
+
+/* Scheduling policies.  TDPIPE = the paper's method (§3.3-§3.5); PPSB_* are the
+ * naive phase-interleaved PP + separate-batching baselines:
+ * PRIO issues a prefill whenever one is admissible, ALT alternates. */
+#define TD_POLICY_TDPIPE 0
+#define TD_POLICY_PPSB_PRIO 1
+#define TD_POLICY_PPSB_ALT 2
+
+/* Executors.  CUDA = the real sm_100a path.  NULL = controller only (no GPU
+ * touched; micro-batches complete logically) -- used to test the scheduler. */
+#define TD_EXEC_CUDA 0
+#define TD_EXEC_NULL 1
+
+/* Model shape (Llama-style pre-norm decoder; Table 2). */
+typedef struct td_model_shape {
+  int32_t n_layers;
+  int32_t d_model;
+  int32_t n_heads;
+  int32_t n_kv_heads;   /* GQA: must divide n_heads */
+  int32_t d_ffn;
+  int32_t vocab;
+  float rope_theta;     /* 1e4: rotate-half RoPE */
+  float rms_eps;        /* 1e-5 */
+  int32_t max_seq_len;  /* prompt + generated tokens per request */
+} td_model_shape;
+
+typedef struct td_options {
+  int32_t executor;             /* TD_EXEC_CUDA | TD_EXEC_NULL                         */
+  int32_t device;               /* CUDA device of stage 0 (single-process mode)        */
+  int32_t devices_per_stage;    /* 0: all stages on `device`; 1: stage s on device+s   */
+  int32_t block_size;           /* KV block (page) size in tokens, B (default 16)      */
+  int64_t kv_blocks;            /* C; 0 = fill HBM (min over stages)                   */
+  double hbm_reserve_frac;      /* HBM kept free when kv_blocks = 0 (default 0.06)     */
+  int32_t prefill_token_budget; /* tokens per prefill micro-batch (2048)  */
+  int32_t max_batch_seqs;       /* max sequences per micro-batch (default 1024)        */
+  int32_t fp_stride;            /* futurePoints stride (32)              */
+  int32_t fp_horizon;           /* futurePoints horizon (1024)           */
+  int32_t policy;               /* TD_POLICY_*                                         */
+  int32_t steal;                /* inter-batch work stealing on/off     */
+  int32_t alg1_check_before_launch; /* 0 = verbatim Alg.1 (launch precedes check)     */
+  int32_t eq2_bubble_scale;     /* sigma in Eq.2's bubble: 1 = verbatim, S-1 = depth   */
+  uint64_t weight_seed;         /* F9 counter-based weight recipe seed                 */
+  const char* profile_csv;      /* frozen profile table "D,b,ns"/"P,k,ns"; NULL = none */
+  int32_t log_decisions;        /* keep the decision log (td_get_log)                  */
+  int32_t record_logits;        /* keep fp32 logits of every generated token           */
+  /* multi-process pipeline (one process per GPU, SPMD runtime PAPER.md:310-314) */
+  int32_t world_size;           /* 1 = single process                                  */
+  int32_t rank;                 /* this process's stage                                */
+  const void* nccl_ids;         /* 2 x 128-byte ncclUniqueId (fwd, bwd) from td_nccl_ids */
+} td_options;
+
+typedef struct td_run_stats {
+  int64_t n_requests;
+  int64_t prompt_tokens;        /* prompt tokens processed (incl. recompute)           */
+  int64_t generated_tokens;
+  int64_t makespan_ns;          /* first prefill launch -> last return  */
+  double gen_tokens_per_s;
+  double total_tokens_per_s;    /* (prompt + generated) / makespan      */
+  double bubble_frac;           /* 1 - sum_s busy_s / (S * makespan)                   */
+  int64_t n_microbatches;
+  int64_t n_prefill_mb;
+  int64_t n_decode_mb;
+  int64_t n_p2d;
+  int64_t n_d2p;
+  int64_t n_stolen;
+  int64_t n_evicted;
+  int64_t gpu_launches;         /* kernels this process launched during td_run         */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+  int64_t busy_ns[8];           /* per-stage busy time (first 8 stages)                */
+} td_run_stats;
+
+/* A single micro-batch for td_stage_forward (testing entry point). */
+#define TD_BATCH_PREFILL 0
+#define TD_BATCH_DECODE 1
+typedef struct td_batch {
+  int32_t kind;                 /* TD_BATCH_PREFILL | TD_BATCH_DECODE                  */
+  int32_t n_seqs;
+  const int32_t* seq_slot;      /* [n] request slot (0 .. max_requests-1), KV owner    */
+  const int32_t* q_start;       /* [n] absolute position of the first new token        */
+  const int32_t* q_len;         /* [n] new tokens (prefill: L; decode: 1)              */
+  const int32_t* block_table;   /* [n * max_blocks] physical KV block ids              */
+  int32_t max_blocks;
+} td_batch;
+
+/* Fill `o` with defaults (executor CUDA, device 0, B=16, budget 2048, ...). */
+void td_default_options(td_options* o);
+
+/* Create a context: validate the shape (n_stages <= n_layers, SPEC.md:118;
+ * n_kv_heads | n_heads; head_dim in {16,32,64,128}), partition layers
+ * (balanced, remainder to earlier stages), allocate and
+ * hash-initialise the weights on device, size the paged KV pool.
+ * Errors: TD_EINVAL, TD_ENOMEM, TD_ECUDA, TD_ENCCL. */
+td_status td_create(const td_model_shape* shape, int32_t n_stages, const td_options* opts,
+                    struct td_ctx** out);
+void td_destroy(struct td_ctx* ctx);
+const char* td_last_error(const struct td_ctx* ctx);
+
+/* Submit one request (offline request set).  The prompt is
+ * copied.  predicted_len < 1 is clamped to 1; max_new_tokens
+ * (>= 1) is the stop length (EOS is disabled for random weights).
+ * Returns the request id (submission order = FIFO order) or a negative
+ * td_status: TD_ERANGE if n_prompt + max_new_tokens > max_seq_len or the
+ * request alone exceeds the KV pool. */
+int64_t td_submit(struct td_ctx* ctx, const int32_t* prompt, int32_t n_prompt,
+                  int32_t predicted_len, int32_t max_new_tokens);
+
+/* Stage the submitted prompts in device memory (H2D) so that td_run starts
+ * with inputs resident in HBM.  Optional: td_run calls it if needed. */
+td_status td_upload(struct td_ctx* ctx);
+
+/* Run every submitted request to completion (blocks).  Generated tokens stay
+ * on device until td_get_output.  st may be NULL. */
+td_status td_run(struct td_ctx* ctx, td_run_stats* st);
+
+/* Generated tokens of request `id` into caller buffer `buf` (capacity `cap`);
+ * *n = number of tokens.  TD_ERANGE if cap < *n (n still set). */
+td_status td_get_output(struct td_ctx* ctx, int64_t id, int32_t* buf, int32_t cap, int32_t* n);
+
+/* All outputs at once: out[id * stride + j] for j < n_out[id]; one D2H copy. */
+td_status td_get_outputs(struct td_ctx* ctx, int32_t* out, int32_t stride, int32_t* n_out);
+
+/* fp32 logits [n_steps, vocab] of request `id` (requires record_logits). */
+td_status td_get_logits(struct td_ctx* ctx, int64_t id, float* buf, int64_t cap, int32_t* n_steps);
+
+/* Forget all submitted requests (outputs, logs) and clear KV; weights kept. */
+td_status td_reset(struct td_ctx* ctx);
+
+/* Run ONE pipeline stage on one micro-batch (testing):
+ * in  = stage 0: int32 tokens [T]; else fp32 residual [T, d_model]
+ * out = last stage: fp32 logits [n_seqs, vocab] of each sequence's last token;
+ *       else fp32 residual [T, d_model]
+ * T = sum(q_len).  Reads/writes the stage's KV pool through block_table, so a
+ * DECODE call follows a PREFILL into the same blocks.  Host pointers. */
+td_status td_stage_forward(struct td_ctx* ctx, int32_t stage, const td_batch* b,
+                           const void* in, void* out);
+
+/* Zero every stage's KV pool. */
+td_status td_kv_reset(struct td_ctx* ctx);
+
+/* Measure per-stage decode-step ns for b = 1..b_max at context ctx_len and
+ * prefill ns for k = 1..k_max tokens (sampled grid, linearly interpolated),
+ * write the dense CSV read through td_options.profile_csv (§3.5 "we profile
+ * the execution time") and load it into this ctx. */
+td_status td_profile(struct td_ctx* ctx, const char* out_csv, int32_t b_max, int32_t k_max,
+                     int32_t ctx_len);
+
+/* Load a profile CSV into this ctx (replaces the current table). */
+td_status td_load_profile(struct td_ctx* ctx, const char* csv);
+
+/* Decision log of the last td_run, '\n'-separated.
+ * Copies min(cap, need) bytes; *need = full length (without NUL). */
+td_status td_get_log(struct td_ctx* ctx, char* buf, size_t cap, size_t* need);
+
+/* Model / pool facts: kv_blocks, layers of `stage`, weight bytes per stage. */
+td_status td_info(struct td_ctx* ctx, int64_t* kv_blocks, int32_t* n_stages,
+                  int64_t* weight_bytes_stage0, int64_t* kv_bytes_per_block);
+
+/* Per-kernel timing over the last td_run (CUDA events on the launching
+ * stream, measured when td_options.executor = CUDA and timing is enabled with
+ * td_set_timing(ctx, 1)).  name = kernel class ("decode_attn", "gemm_qkv", ...). */
+td_status td_set_timing(struct td_ctx* ctx, int32_t on);
+td_status td_get_timing(struct td_ctx* ctx, const char* name, int64_t* launches,
+                        double* total_ms, double* bytes, double* flops);
+
+/* Generate the two ncclUniqueIds (256 bytes) rank 0 shares with all ranks. */
+td_status td_nccl_ids(void* out256);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDPIPE_H_ */

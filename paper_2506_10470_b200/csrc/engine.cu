@@ -1,0 +1,815 @@
+// engine.cu -- single-process CUDA execution plane.
+//
+// Executes the micro-batch plan the controller emits, in launch order, on one
+// stream of one sm_100a device.  All pipeline stages of a micro-batch run back
+// to back; the stage hand-off is the fp32 residual buffer (SURVEY.md §0.1-6:
+// keep the residual stream in fp32).  Generated tokens stay on device: the last
+// stage writes argmax tokens into the token arena at the request's next
+// position and stage 0 gathers them from there, so the host never waits on the
+// GPU inside td_run (the controller's decisions depend only on logical events,
+// SURVEY.md §0.1-7, so the host runs ahead, bounded by the metadata ring).
+//
+// HBM layout (per device):
+//   weights  per layer: Wqkv [(H+2Hkv)hd, d] (q/k rotate-half pairs interleaved),
+//            Wo [d, H hd], Wgu [2F, d] (gate/up rows interleaved), Wd [d, F],
+//            g1, g2 [d]; E [V, d]; gf [d]; Wlm [V, d]      (bf16, K-major)
+//   KV pool  per layer: [C blocks][K|V][Hkv][16][hd] bf16
+//   arena    int32 tokens, request r at offset off[r]: prompt ++ generated
+//   work     x fp32 [T, d]; a bf16 [T, d]; q, o bf16 [T, H hd]; h bf16 [T, F];
+//            logits fp32 [n, V]; split-KV partials
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "kernels/kernels.h"
+
+namespace tdp {
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                          \
+      error = std::string(#x) + ": " + cudaGetErrorString(e_);                        \
+      return TD_ECUDA;                                                                \
+    }                                                                                 \
+  } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct LayerW {
+  bf16 *wqkv, *wo, *wgu, *wd, *g1, *g2;
+};
+
+// Per-micro-batch metadata (host-built, one H2D copy): int32 arrays.
+struct Meta {
+  int n = 0, T = 0, maxblk = 0, max_ctx = 0, prefill = 0;
+  // offsets (in int32 units) into the packed buffer
+  int o_ctx, o_tokidx, o_pos, o_slot, o_seq, o_last, o_outpos, o_bt;
+  int total = 0;
+};
+
+struct TimedLaunch {
+  cudaEvent_t a, b;
+  int cls;
+  double bytes, flops;
+};
+
+class CudaEngine : public Engine {
+ public:
+  ~CudaEngine() override { release(); }
+
+  td_status init(const td_model_shape& s, int n_stages, const td_options& o);
+  int64_t kv_blocks() const override { return C_; }
+  int64_t kv_bytes_per_block() const override { return kv_block_bytes_layer_ * s_.n_layers; }
+  int64_t weight_bytes_stage0() const override { return weight_bytes_; }
+  td_status upload(const std::vector<HostReq>& reqs) override;
+  bool uploaded() const override { return uploaded_; }
+  td_status begin_run(const std::vector<HostReq>& reqs, bool record_logits) override;
+  int launch(const MicroBatch& mb, const std::vector<Req>& reqs) override;
+  td_status end_run(td_run_stats* st) override;
+  td_status get_outputs(const std::vector<HostReq>& reqs, const std::vector<int>& n_out,
+                        std::vector<std::vector<int32_t>>* out) override;
+  td_status get_logits(int64_t rid, std::vector<float>* out, int* n_steps) override;
+  td_status stage_forward(int stage, const td_batch& b, const void* in, void* out) override;
+  td_status kv_reset() override;
+  td_status profile(int b_max, int k_max, int ctx_len, std::vector<int64_t>* tdec,
+                    std::vector<int64_t>* tpre) override;
+  void set_timing(bool on) override { timing_ = on; }
+  bool get_timing(const std::string& name, KernelTiming* t) override;
+
+ private:
+  void release();
+  td_status ensure_work(int64_t T, int64_t n, int64_t maxblk);
+  // build metadata into ring slot `r`; returns the packed layout
+  Meta build_meta(int r, bool prefill, int n, const int* q_start, const int* q_len, const int32_t* arena_off,
+                  const std::vector<const std::vector<int32_t>*>& blocks, const int32_t* bt_flat, int bt_stride);
+  td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena);
+  td_status run_microbatch(const Meta& M, const int32_t* dmeta, int32_t* arena);
+  void tbegin(int cls);
+  void tend(int cls, double bytes, double flops);
+  int ring_acquire();
+
+  td_model_shape s_{};
+  td_options o_{};
+  int S_ = 1, hd_ = 0, H_ = 0, Hkv_ = 0, d_ = 0, F_ = 0, V_ = 0;
+  std::vector<int> stage_l0_, stage_l1_;
+  int dev_ = 0;
+  cudaStream_t st_ = nullptr;
+  // weights
+  bf16* wbuf_ = nullptr;
+  int64_t weight_bytes_ = 0;
+  std::vector<LayerW> L_;
+  bf16 *E_ = nullptr, *gf_ = nullptr, *Wlm_ = nullptr;
+  // kv
+  bf16* kv_ = nullptr;
+  int64_t C_ = 0, kv_block_bytes_layer_ = 0;
+  float* rope_ = nullptr;
+  // work
+  int64_t capT_ = 0, capN_ = 0, capBlk_ = 0;
+  float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
+  bf16 *a_ = nullptr, *q_ = nullptr, *ob_ = nullptr, *h_ = nullptr;
+  int max_splits_cap_ = 0;
+  // arena
+  int32_t* arena_ = nullptr;
+  int64_t arena_cap_ = 0;
+  std::vector<int32_t> arena_off_;
+  bool uploaded_ = false;
+  // metadata ring
+  static constexpr int kRing = 8;
+  int32_t* hmeta_[kRing] = {};
+  int32_t* dmeta_[kRing] = {};
+  cudaEvent_t ring_ev_[kRing] = {};
+  bool ring_used_[kRing] = {};
+  int64_t meta_cap_ = 0;
+  int ring_next_ = 0;
+  // run bookkeeping
+  cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
+  bool started_ = false;
+  bool record_ = false;
+  std::vector<std::vector<float>> rec_;
+  float* hlogits_ = nullptr;
+  int64_t hlogits_cap_ = 0;
+  int64_t launches_ = 0, h2d_bytes_ = 0;
+  // timing
+  bool timing_ = false;
+  std::vector<TimedLaunch> timed_;
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_used_ = 0;
+  std::map<std::string, KernelTiming> timing_acc_;
+  std::vector<std::string> cls_names_{"decode_attn", "prefill_attn", "gemm_qkv", "gemm_o", "gemm_gu",
+                                      "gemm_down", "lm_head", "norm", "stage", "mb"};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev_;
+};
+
+enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
+
+// --------------------------------------------------------------------- init
+td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_options& o) {
+  s_ = s;
+  o_ = o;
+  S_ = n_stages;
+  d_ = s.d_model;
+  H_ = s.n_heads;
+  Hkv_ = s.n_kv_heads;
+  hd_ = d_ / H_;
+  F_ = s.d_ffn;
+  V_ = s.vocab;
+  if (o.world_size > 1) { error = "multi-process pipeline requires the NCCL engine"; return TD_EINVAL; }
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (o.device < 0 || o.device >= ndev) { error = "bad device"; return TD_ECUDA; }
+  dev_ = o.device;
+  CK(cudaSetDevice(dev_));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev_));
+  if (prop.major != 10) { error = "needs an sm_100 (B200) device"; return TD_ECUDA; }
+  CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  // layer partition: balanced, remainder to earlier stages
+  int q = s.n_layers / S_, r = s.n_layers % S_, l = 0;
+  for (int i = 0; i < S_; ++i) {
+    stage_l0_.push_back(l);
+    l += q + (i < r ? 1 : 0);
+    stage_l1_.push_back(l);
+  }
+  // ---- weights
+  const int64_t nqkv = (int64_t)(H_ + 2 * Hkv_) * hd_;
+  const int64_t per_layer = nqkv * d_ + (int64_t)d_ * H_ * hd_ + 2LL * F_ * d_ + (int64_t)d_ * F_ + 2LL * d_;
+  const int64_t glob = (int64_t)V_ * d_ * 2 + d_;
+  const int64_t nelem = per_layer * s.n_layers + glob;
+  weight_bytes_ = nelem * 2;
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  if ((double)weight_bytes_ > 0.9 * fr) { error = "weights do not fit"; return TD_ENOMEM; }
+  CK(cudaMalloc(&wbuf_, nelem * 2));
+  bf16* p = wbuf_;
+  auto take = [&](int64_t n) { bf16* r = p; p += n; return r; };
+  const int L = s.n_layers;
+  auto tid = [&](int layer, int which) { return 1 + 9 * layer + which; };
+  for (int i = 0; i < L; ++i) {
+    LayerW w;
+    w.wqkv = take(nqkv * d_);
+    w.wo = take((int64_t)d_ * H_ * hd_);
+    w.wgu = take(2LL * F_ * d_);
+    w.wd = take((int64_t)d_ * F_);
+    w.g1 = take(d_);
+    w.g2 = take(d_);
+    L_.push_back(w);
+    auto sc = [](int fan_in) { return std::sqrt(3.0f / (float)fan_in); };
+    InitSpec a{kMapQKV, kInitProj, (int)nqkv, d_, tid(i, 1), tid(i, 2), tid(i, 3), H_, Hkv_, hd_, sc(d_)};
+    launch_init(w.wqkv, a, o.weight_seed, st_);
+    InitSpec b{kMapIdentity, kInitProj, d_, H_ * hd_, tid(i, 4), 0, 0, 0, 0, 0, sc(H_ * hd_)};
+    launch_init(w.wo, b, o.weight_seed, st_);
+    InitSpec c{kMapGateUp, kInitProj, 2 * F_, d_, tid(i, 6), tid(i, 7), 0, 0, 0, 0, sc(d_)};
+    launch_init(w.wgu, c, o.weight_seed, st_);
+    InitSpec dd{kMapIdentity, kInitProj, d_, F_, tid(i, 8), 0, 0, 0, 0, 0, sc(F_)};
+    launch_init(w.wd, dd, o.weight_seed, st_);
+    InitSpec g1{kMapIdentity, kInitNorm, 1, d_, tid(i, 0), 0, 0, 0, 0, 0, 0.f};
+    launch_init(w.g1, g1, o.weight_seed, st_);
+    InitSpec g2{kMapIdentity, kInitNorm, 1, d_, tid(i, 5), 0, 0, 0, 0, 0, 0.f};
+    launch_init(w.g2, g2, o.weight_seed, st_);
+  }
+  E_ = take((int64_t)V_ * d_);
+  Wlm_ = take((int64_t)V_ * d_);
+  gf_ = take(d_);
+  InitSpec e{kMapIdentity, kInitEmbed, V_, d_, 0, 0, 0, 0, 0, 0, 0.f};
+  launch_init(E_, e, o.weight_seed, st_);
+  InitSpec lm{kMapIdentity, kInitProj, V_, d_, 2 + 9 * L, 0, 0, 0, 0, 0, std::sqrt(3.0f / (float)d_)};
+  launch_init(Wlm_, lm, o.weight_seed, st_);
+  InitSpec gf{kMapIdentity, kInitNorm, 1, d_, 1 + 9 * L, 0, 0, 0, 0, 0, 0.f};
+  launch_init(gf_, gf, o.weight_seed, st_);
+  CK(cudaGetLastError());
+  // ---- RoPE table [max_seq_len][hd/2] (cos, sin), from double
+  {
+    const int P = s.max_seq_len, half = hd_ / 2;
+    std::vector<float> cs((size_t)P * half * 2);
+    for (int pp = 0; pp < P; ++pp)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow((double)s.rope_theta, -2.0 * i / hd_);
+        const double ang = (double)pp * inv;
+        cs[((size_t)pp * half + i) * 2] = (float)std::cos(ang);
+        cs[((size_t)pp * half + i) * 2 + 1] = (float)std::sin(ang);
+      }
+    CK(cudaMalloc(&rope_, cs.size() * 4));
+    CK(cudaMemcpyAsync(rope_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+  // ---- work buffers for a default capacity, then the KV pool fills HBM
+  const int64_t T0 = std::max<int64_t>(o.prefill_token_budget, s.max_seq_len);
+  if (td_status e2 = ensure_work(T0, std::min<int64_t>(o.max_batch_seqs, 1024), cdiv(s.max_seq_len, 16))) return e2;
+  kv_block_bytes_layer_ = 2LL * Hkv_ * 16 * hd_ * 2;
+  const int64_t per_block = kv_block_bytes_layer_ * L;
+  if (o.kv_blocks > 0) {
+    C_ = o.kv_blocks;
+  } else {
+    CK(cudaMemGetInfo(&fr, &tot));
+    const double avail = (double)fr - o.hbm_reserve_frac * (double)tot - 512.0 * (1 << 20);
+    C_ = (int64_t)(avail / (double)per_block);
+  }
+  if (C_ < 1) { error = "no room for the KV pool"; return TD_ENOMEM; }
+  if (cudaMalloc(&kv_, C_ * per_block) != cudaSuccess) { error = "KV pool allocation failed"; return TD_ENOMEM; }
+  CK(cudaMemsetAsync(kv_, 0, C_ * per_block, st_));
+  CK(cudaEventCreate(&ev_start_));
+  CK(cudaEventCreate(&ev_end_));
+  for (int i = 0; i < kRing; ++i) CK(cudaEventCreateWithFlags(&ring_ev_[i], cudaEventDisableTiming));
+  CK(cudaStreamSynchronize(st_));
+  return TD_OK;
+}
+
+void CudaEngine::release() {
+  if (st_) cudaStreamSynchronize(st_);
+  cudaFree(wbuf_);
+  cudaFree(kv_);
+  cudaFree(rope_);
+  cudaFree(x_);
+  cudaFree(logits_);
+  cudaFree(part_);
+  cudaFree(a_);
+  cudaFree(q_);
+  cudaFree(ob_);
+  cudaFree(h_);
+  cudaFree(arena_);
+  for (int i = 0; i < kRing; ++i) {
+    if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
+    cudaFree(dmeta_[i]);
+    if (ring_ev_[i]) cudaEventDestroy(ring_ev_[i]);
+  }
+  if (hlogits_) cudaFreeHost(hlogits_);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto& pr : stage_ev_) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  if (ev_start_) cudaEventDestroy(ev_start_);
+  if (ev_end_) cudaEventDestroy(ev_end_);
+  if (st_) cudaStreamDestroy(st_);
+  st_ = nullptr;
+}
+
+td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
+  T = std::max(T, n);
+  if (T <= capT_ && n <= capN_ && maxblk <= capBlk_) return TD_OK;
+  CK(cudaStreamSynchronize(st_));
+  T = std::max(T, capT_);
+  n = std::max(n, capN_);
+  maxblk = std::max(maxblk, capBlk_);
+  cudaFree(x_); cudaFree(a_); cudaFree(q_); cudaFree(ob_); cudaFree(h_); cudaFree(logits_); cudaFree(part_);
+  CK(cudaMalloc(&x_, T * d_ * 4));
+  CK(cudaMalloc(&a_, T * d_ * 2));
+  CK(cudaMalloc(&q_, T * H_ * hd_ * 2));
+  CK(cudaMalloc(&ob_, T * H_ * hd_ * 2));
+  CK(cudaMalloc(&h_, T * F_ * 2));
+  CK(cudaMalloc(&logits_, n * V_ * 4));
+  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 512);
+  CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
+  // metadata ring: per seq 5 ints + bt, per token 4 ints, header
+  const int64_t need = 16 + 5 * n + 2 + n * maxblk + 4 * T + 64;
+  if (need > meta_cap_) {
+    for (int i = 0; i < kRing; ++i) {
+      if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
+      cudaFree(dmeta_[i]);
+      CK(cudaMallocHost(&hmeta_[i], need * 4));
+      CK(cudaMalloc(&dmeta_[i], need * 4));
+    }
+    meta_cap_ = need;
+  }
+  capT_ = T;
+  capN_ = n;
+  capBlk_ = maxblk;
+  return TD_OK;
+}
+
+// -------------------------------------------------------------------- ring
+int CudaEngine::ring_acquire() {
+  const int r = ring_next_;
+  ring_next_ = (ring_next_ + 1) % kRing;
+  if (ring_used_[r]) cudaEventSynchronize(ring_ev_[r]);   // bound the host run-ahead
+  ring_used_[r] = true;
+  return r;
+}
+
+Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, const int* q_len,
+                            const int32_t* arena_off, const std::vector<const std::vector<int32_t>*>& blocks,
+                            const int32_t* bt_flat, int bt_stride) {
+  Meta M;
+  M.n = n;
+  M.prefill = prefill ? 1 : 0;
+  int T = 0, maxblk = 1, max_ctx = 1;
+  for (int i = 0; i < n; ++i) {
+    T += q_len[i];
+    const int ctx = q_start[i] + q_len[i];
+    max_ctx = std::max(max_ctx, ctx);
+    maxblk = std::max<int>(maxblk, (int)cdiv(ctx, 16));
+  }
+  M.T = T;
+  M.maxblk = maxblk;
+  M.max_ctx = max_ctx;
+  int off = 0;
+  M.o_ctx = off; off += n;
+  M.o_last = off; off += n;
+  M.o_outpos = off; off += n;
+  M.o_tokidx = off; off += T;
+  M.o_pos = off; off += T;
+  M.o_slot = off; off += T;
+  M.o_seq = off; off += T;
+  M.o_bt = off; off += n * maxblk;
+  M.total = off;
+  int32_t* h = hmeta_[r];
+  int t = 0;
+  for (int i = 0; i < n; ++i) {
+    const int ctx = q_start[i] + q_len[i];
+    h[M.o_ctx + i] = ctx;
+    const int nb = (int)cdiv(ctx, 16);
+    int32_t* bt = h + M.o_bt + (int64_t)i * maxblk;
+    for (int b = 0; b < maxblk; ++b)
+      bt[b] = b < nb ? (blocks.empty() ? bt_flat[(int64_t)i * bt_stride + b] : (*blocks[i])[b]) : 0;
+    for (int j = 0; j < q_len[i]; ++j, ++t) {
+      const int pos = q_start[i] + j;
+      h[M.o_tokidx + t] = arena_off ? arena_off[i] + pos : t;
+      h[M.o_pos + t] = pos;
+      h[M.o_slot + t] = bt[pos >> 4] * 16 + (pos & 15);
+      h[M.o_seq + t] = i;
+    }
+    h[M.o_last + i] = t - 1;
+    h[M.o_outpos + i] = arena_off ? arena_off[i] + ctx : 0;
+  }
+  return M;
+}
+
+// ------------------------------------------------------------------ timing
+void CudaEngine::tbegin(int cls) {
+  if (!timing_) return;
+  if (ev_used_ + 2 > ev_pool_.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool_.push_back(e);
+    }
+  }
+  TimedLaunch tl;
+  tl.a = ev_pool_[ev_used_++];
+  tl.b = ev_pool_[ev_used_++];
+  tl.cls = cls;
+  tl.bytes = tl.flops = 0;
+  cudaEventRecord(tl.a, st_);
+  timed_.push_back(tl);
+}
+void CudaEngine::tend(int cls, double bytes, double flops) {
+  if (!timing_) return;
+  TimedLaunch& tl = timed_.back();
+  (void)cls;
+  tl.bytes = bytes;
+  tl.flops = flops;
+  cudaEventRecord(tl.b, st_);
+}
+
+bool CudaEngine::get_timing(const std::string& name, KernelTiming* t) {
+  auto it = timing_acc_.find(name);
+  if (it == timing_acc_.end()) { *t = KernelTiming(); return true; }
+  *t = it->second;
+  return true;
+}
+
+// ------------------------------------------------------------------ forward
+td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int32_t* arena) {
+  const int T = M.T, n = M.n;
+  const int nqkv = (H_ + 2 * Hkv_) * hd_;
+  const float eps = s_.rms_eps;
+  if (stage == 0) {
+    launch_embed(arena, dm + M.o_tokidx, E_, x_, T, d_, st_);
+    launches_++;
+  }
+  for (int l = stage_l0_[stage]; l < stage_l1_[stage]; ++l) {
+    const LayerW& w = L_[l];
+    bf16* kvl = kv_ + (int64_t)l * C_ * (kv_block_bytes_layer_ / 2);
+    launch_rmsnorm(x_, w.g1, a_, nullptr, T, d_, eps, st_);
+    EpiParams ep{};
+    ep.mode = kEpiQKV;
+    ep.out_bf16 = q_;
+    ep.kcache = kvl;
+    ep.pos = dm + M.o_pos;
+    ep.slot = dm + M.o_slot;
+    ep.rope_cs = rope_;
+    ep.H = H_;
+    ep.Hkv = Hkv_;
+    ep.hd = hd_;
+    tbegin(cQKV);
+    launch_gemm(a_, w.wqkv, T, nqkv, d_, ep, st_);
+    tend(cQKV, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
+    if (M.prefill) {
+      PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_};
+      tbegin(cPreAttn);
+      launch_prefill_attn(pp, st_);
+      tend(cPreAttn, 0, 0);
+      launches_++;
+    } else {
+      const int ms = (int)cdiv(M.max_ctx, 512);
+      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_};
+      tbegin(cDecAttn);
+      launch_decode_attn(dp, st_);
+      tend(cDecAttn, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
+      launches_ += ms > 1 ? 2 : 1;
+    }
+    EpiParams eo{};
+    eo.mode = kEpiResid;
+    eo.out_f32 = x_;
+    eo.ldo = d_;
+    tbegin(cO);
+    launch_gemm(ob_, w.wo, T, d_, H_ * hd_, eo, st_);
+    tend(cO, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
+    launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
+    EpiParams eg{};
+    eg.mode = kEpiSwiGLU;
+    eg.out_bf16 = h_;
+    tbegin(cGU);
+    launch_gemm(a_, w.wgu, T, 2 * F_, d_, eg, st_);
+    tend(cGU, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
+    EpiParams ed{};
+    ed.mode = kEpiResid;
+    ed.out_f32 = x_;
+    ed.ldo = d_;
+    tbegin(cDown);
+    launch_gemm(h_, w.wd, T, d_, F_, ed, st_);
+    tend(cDown, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
+    launches_ += 6;
+  }
+  if (stage == S_ - 1) {
+    launch_rmsnorm(x_, gf_, a_, dm + M.o_last, n, d_, eps, st_);
+    EpiParams el{};
+    el.mode = kEpiF32;
+    el.out_f32 = logits_;
+    el.ldo = V_;
+    tbegin(cLM);
+    launch_gemm(a_, Wlm_, n, V_, d_, el, st_);
+    tend(cLM, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
+    launches_ += 2;
+    if (arena) {
+      launch_argmax(logits_, n, V_, arena, dm + M.o_outpos, st_);
+      launches_++;
+    }
+  }
+  return TD_OK;
+}
+
+td_status CudaEngine::run_microbatch(const Meta& M, const int32_t* dm, int32_t* arena) {
+  for (int s = 0; s < S_; ++s) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (timing_) {
+      tbegin(cStage);
+    }
+    if (td_status e = run_stage(s, M, dm, arena)) return e;
+    if (timing_) tend(cStage, 0, 0);
+    (void)a;
+    (void)b;
+  }
+  return TD_OK;
+}
+
+// ------------------------------------------------------------------- runs
+td_status CudaEngine::upload(const std::vector<HostReq>& reqs) {
+  int64_t total = 0;
+  arena_off_.resize(reqs.size());
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    arena_off_[i] = (int32_t)total;
+    total += (int64_t)reqs[i].prompt.size() + reqs[i].max_new + 1;
+  }
+  if (total > INT32_MAX) { error = "token arena too large"; return TD_ERANGE; }
+  if (total > arena_cap_) {
+    CK(cudaStreamSynchronize(st_));
+    cudaFree(arena_);
+    CK(cudaMalloc(&arena_, std::max<int64_t>(total, 1) * 4));
+    arena_cap_ = total;
+  }
+  std::vector<int32_t> h((size_t)std::max<int64_t>(total, 1), 0);
+  for (size_t i = 0; i < reqs.size(); ++i)
+    std::memcpy(h.data() + arena_off_[i], reqs[i].prompt.data(), reqs[i].prompt.size() * 4);
+  CK(cudaMemcpyAsync(arena_, h.data(), total * 4, cudaMemcpyHostToDevice, st_));
+  CK(cudaStreamSynchronize(st_));
+  h2d_bytes_ = total * 4;
+  uploaded_ = true;
+  return TD_OK;
+}
+
+td_status CudaEngine::begin_run(const std::vector<HostReq>& reqs, bool record_logits) {
+  CK(cudaSetDevice(dev_));
+  if (!uploaded_ || arena_off_.size() != reqs.size()) {
+    if (td_status e = upload(reqs)) return e;
+  }
+  int64_t maxL = 1;
+  for (auto& r : reqs) maxL = std::max<int64_t>(maxL, (int64_t)r.prompt.size() + r.max_new);
+  const int64_t T = std::max<int64_t>(o_.prefill_token_budget, maxL);
+  if (td_status e = ensure_work(T, std::max<int64_t>((int64_t)reqs.size(), 1), cdiv(maxL + 1, 16))) return e;
+  record_ = record_logits;
+  rec_.assign(record_logits ? reqs.size() : 0, {});
+  launches_ = 0;
+  timed_.clear();
+  ev_used_ = 0;
+  timing_acc_.clear();
+  started_ = false;
+  for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
+  return TD_OK;
+}
+
+int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
+  const int n = (int)mb.members.size();
+  if (!started_) {
+    cudaEventRecord(ev_start_, st_);
+    started_ = true;
+  }
+  std::vector<int32_t> aoff(n);
+  std::vector<const std::vector<int32_t>*> blocks(n);
+  for (int i = 0; i < n; ++i) {
+    aoff[i] = arena_off_[mb.members[i]];
+    blocks[i] = &reqs[mb.members[i]].blocks;
+  }
+  {
+    int64_t T = 0, mb_blk = 1;
+    for (int i = 0; i < n; ++i) {
+      T += mb.q_len[i];
+      mb_blk = std::max<int64_t>(mb_blk, cdiv(mb.q_start[i] + mb.q_len[i], 16));
+    }
+    if (T > capT_ || mb_blk > capBlk_ || n > capN_) {
+      if (ensure_work(T, n, mb_blk)) return TD_ECUDA;
+      for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
+    }
+  }
+  const int r = ring_acquire();
+  Meta M = build_meta(r, mb.kind == 'P', n, mb.q_start.data(), mb.q_len.data(), aoff.data(), blocks, nullptr, 0);
+  if (cudaMemcpyAsync(dmeta_[r], hmeta_[r], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_) != cudaSuccess) {
+    error = "metadata H2D failed";
+    return TD_ECUDA;
+  }
+  h2d_bytes_ += (int64_t)M.total * 4;
+  const size_t t0 = timed_.size();
+  if (td_status e = run_microbatch(M, dmeta_[r], arena_)) return e;
+  if (timing_) {
+    // algorithmic bytes of decode attention: every context token's K and V
+    // (2*Hkv*hd*2 bytes per layer) + q and o
+    double kvb = 0;
+    for (int i = 0; i < n; ++i) kvb += (double)(mb.q_start[i] + mb.q_len[i]);
+    kvb = kvb * 2.0 * Hkv_ * hd_ * 2 + 4.0 * n * H_ * hd_;
+    for (size_t k = t0; k < timed_.size(); ++k)
+      if (timed_[k].cls == cDecAttn) timed_[k].bytes = kvb;
+  }
+  cudaEventRecord(ring_ev_[r], st_);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { error = std::string("launch: ") + cudaGetErrorString(e); return TD_ECUDA; }
+  if (record_) {
+    if (hlogits_cap_ < (int64_t)n * V_) {
+      if (hlogits_) cudaFreeHost(hlogits_);
+      cudaMallocHost(&hlogits_, (size_t)n * V_ * 4);
+      hlogits_cap_ = (int64_t)n * V_;
+    }
+    cudaMemcpyAsync(hlogits_, logits_, (size_t)n * V_ * 4, cudaMemcpyDeviceToHost, st_);
+    if (cudaStreamSynchronize(st_) != cudaSuccess) { error = "sync failed"; return TD_ECUDA; }
+    for (int i = 0; i < n; ++i) {
+      auto& v = rec_[mb.members[i]];
+      v.insert(v.end(), hlogits_ + (size_t)i * V_, hlogits_ + (size_t)(i + 1) * V_);
+    }
+  }
+  return 0;
+}
+
+td_status CudaEngine::end_run(td_run_stats* st) {
+  CK(cudaEventRecord(ev_end_, st_));
+  CK(cudaStreamSynchronize(st_));
+  float ms = 0.f;
+  if (started_) CK(cudaEventElapsedTime(&ms, ev_start_, ev_end_));
+  st->makespan_ns = (int64_t)((double)ms * 1e6);
+  double busy = 0;
+  for (auto& tl : timed_) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, tl.a, tl.b);
+    KernelTiming& kt = timing_acc_[cls_names_[tl.cls]];
+    kt.launches++;
+    kt.ms += t;
+    kt.bytes += tl.bytes;
+    kt.flops += tl.flops;
+    if (tl.cls == cStage) busy += t;
+  }
+  if (timing_ && ms > 0) {
+    st->bubble_frac = 1.0 - busy / ((double)S_ * ms);
+    st->busy_ns[0] = (int64_t)(busy * 1e6 / S_);
+  }
+  st->gpu_launches = launches_;
+  st->h2d_bytes = h2d_bytes_;
+  return TD_OK;
+}
+
+td_status CudaEngine::get_outputs(const std::vector<HostReq>& reqs, const std::vector<int>& n_out,
+                                  std::vector<std::vector<int32_t>>* out) {
+  int64_t total = 0;
+  for (size_t i = 0; i < reqs.size(); ++i) total += (int64_t)reqs[i].prompt.size() + reqs[i].max_new + 1;
+  std::vector<int32_t> h((size_t)std::max<int64_t>(total, 1));
+  CK(cudaMemcpyAsync(h.data(), arena_, total * 4, cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  out->assign(reqs.size(), {});
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    const int32_t* base = h.data() + arena_off_[i] + reqs[i].prompt.size();
+    (*out)[i].assign(base, base + n_out[i]);
+  }
+  return TD_OK;
+}
+
+td_status CudaEngine::get_logits(int64_t rid, std::vector<float>* out, int* n_steps) {
+  if (!record_ || rid < 0 || rid >= (int64_t)rec_.size()) { error = "logits not recorded"; return TD_ESTATE; }
+  *out = rec_[rid];
+  *n_steps = (int)(out->size() / V_);
+  return TD_OK;
+}
+
+td_status CudaEngine::kv_reset() {
+  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * s_.n_layers, st_));
+  CK(cudaStreamSynchronize(st_));
+  return TD_OK;
+}
+
+// ----------------------------------------------------------- stage forward
+td_status CudaEngine::stage_forward(int stage, const td_batch& b, const void* in, void* out) {
+  CK(cudaSetDevice(dev_));
+  const int n = b.n_seqs;
+  if (n < 1) { error = "empty batch"; return TD_EINVAL; }
+  int T = 0, maxctx = 1;
+  for (int i = 0; i < n; ++i) {
+    if (b.q_len[i] < 1 || b.q_start[i] < 0) { error = "bad q_len/q_start"; return TD_EINVAL; }
+    if (b.kind == TD_BATCH_DECODE && b.q_len[i] != 1) { error = "decode q_len must be 1"; return TD_EINVAL; }
+    if (b.kind == TD_BATCH_PREFILL && b.q_start[i] != 0) { error = "prefill starts at 0"; return TD_EINVAL; }
+    T += b.q_len[i];
+    maxctx = std::max(maxctx, b.q_start[i] + b.q_len[i]);
+    if (maxctx > s_.max_seq_len) { error = "context > max_seq_len"; return TD_ERANGE; }
+    if (cdiv(b.q_start[i] + b.q_len[i], 16) > b.max_blocks) { error = "block table too short"; return TD_EINVAL; }
+    for (int k = 0; k < cdiv(b.q_start[i] + b.q_len[i], 16); ++k) {
+      const int32_t blk = b.block_table[(int64_t)i * b.max_blocks + k];
+      if (blk < 0 || blk >= C_) { error = "block id out of range"; return TD_ERANGE; }
+    }
+  }
+  if (td_status e = ensure_work(T, n, cdiv(maxctx, 16))) return e;
+  CK(cudaStreamSynchronize(st_));
+  for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
+  const int r = 0;
+  Meta M = build_meta(r, b.kind == TD_BATCH_PREFILL, n, b.q_start, b.q_len, nullptr, {}, b.block_table, b.max_blocks);
+  CK(cudaMemcpyAsync(dmeta_[r], hmeta_[r], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_));
+  int32_t* tok = nullptr;
+  if (stage == 0) {
+    CK(cudaMalloc(&tok, (size_t)T * 4));
+    CK(cudaMemcpyAsync(tok, in, (size_t)T * 4, cudaMemcpyHostToDevice, st_));
+  } else {
+    CK(cudaMemcpyAsync(x_, in, (size_t)T * d_ * 4, cudaMemcpyHostToDevice, st_));
+  }
+  td_status e = run_stage(stage, M, dmeta_[r], tok);
+  if (e == TD_OK) {
+    if (stage == S_ - 1) CK(cudaMemcpyAsync(out, logits_, (size_t)n * V_ * 4, cudaMemcpyDeviceToHost, st_));
+    else CK(cudaMemcpyAsync(out, x_, (size_t)T * d_ * 4, cudaMemcpyDeviceToHost, st_));
+  }
+  CK(cudaStreamSynchronize(st_));
+  CK(cudaGetLastError());
+  if (tok) cudaFree(tok);
+  return e;
+}
+
+// ----------------------------------------------------------------- profile
+// Eq.1 needs "the execution time ... for each batch size":
+// per-stage decode-step ns at a representative context, prefill ns per token
+// count; sampled grid, integer linear interpolation, per-stage max.
+td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int64_t>* tdec,
+                              std::vector<int64_t>* tpre) {
+  CK(cudaSetDevice(dev_));
+  ctx_len = std::min(ctx_len, s_.max_seq_len - 1);
+  const int nb = (int)cdiv(ctx_len, 16);
+  if (td_status e = ensure_work(std::max(k_max, b_max), b_max, nb + 1)) return e;
+  int32_t* tok = nullptr;
+  CK(cudaMalloc(&tok, (size_t)std::max(k_max, b_max) * 4));
+  CK(cudaMemsetAsync(tok, 0, (size_t)std::max(k_max, b_max) * 4, st_));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto time_batch = [&](bool prefill, int n, const std::vector<int>& qs, const std::vector<int>& ql,
+                        int64_t* out_ns) -> td_status {
+    std::vector<int32_t> bt((size_t)n * (nb + 1));
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k <= nb; ++k) bt[(size_t)i * (nb + 1) + k] = (int32_t)(((int64_t)i * (nb + 1) + k) % C_);
+    for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
+    Meta M = build_meta(0, prefill, n, qs.data(), ql.data(), nullptr, {}, bt.data(), nb + 1);
+    CK(cudaMemcpyAsync(dmeta_[0], hmeta_[0], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_));
+    int64_t worst = 0;
+    for (int s = 0; s < S_; ++s) {
+      std::vector<float> ts;
+      for (int rep = 0; rep < 6; ++rep) {
+        CK(cudaEventRecord(e0, st_));
+        if (td_status e = run_stage(s, M, dmeta_[0], tok)) return e;
+        CK(cudaEventRecord(e1, st_));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep >= 2) ts.push_back(ms);
+      }
+      std::sort(ts.begin(), ts.end());
+      worst = std::max<int64_t>(worst, (int64_t)(ts[ts.size() / 2] * 1e6));
+    }
+    *out_ns = worst;
+    return TD_OK;
+  };
+  const bool saved = timing_;
+  timing_ = false;
+  std::vector<int> bgrid;
+  for (int b = 1; b <= b_max; b = b < 16 ? b * 2 : b + (b < 256 ? 16 : 64)) bgrid.push_back(b);
+  if (bgrid.back() != b_max) bgrid.push_back(b_max);
+  std::vector<int64_t> bval;
+  for (int b : bgrid) {
+    std::vector<int> qs(b, ctx_len - 1), ql(b, 1);
+    int64_t ns = 0;
+    if (td_status e = time_batch(false, b, qs, ql, &ns)) return e;
+    bval.push_back(ns);
+  }
+  std::vector<int> kgrid;
+  for (int k = 16; k < k_max; k *= 2) kgrid.push_back(k);
+  kgrid.push_back(k_max);
+  std::vector<int64_t> kval;
+  for (int k : kgrid) {
+    std::vector<int> qs, ql;
+    for (int left = k; left > 0; left -= ctx_len) { qs.push_back(0); ql.push_back(std::min(left, ctx_len)); }
+    int64_t ns = 0;
+    if (td_status e = time_batch(true, (int)qs.size(), qs, ql, &ns)) return e;
+    kval.push_back(ns);
+  }
+  timing_ = saved;
+  auto interp = [](const std::vector<int>& g, const std::vector<int64_t>& v, int maxv, std::vector<int64_t>* out) {
+    out->assign(maxv + 1, 0);
+    for (int x = 1; x <= maxv; ++x) {
+      size_t j = 0;
+      while (j + 1 < g.size() && g[j + 1] < x) ++j;
+      if (x <= g[0]) { (*out)[x] = v[0]; continue; }
+      if (j + 1 >= g.size()) { (*out)[x] = v.back(); continue; }
+      const int64_t x0 = g[j], x1 = g[j + 1];
+      (*out)[x] = v[j] + (v[j + 1] - v[j]) * (x - x0) / (x1 - x0);
+    }
+  };
+  interp(bgrid, bval, b_max, tdec);
+  interp(kgrid, kval, k_max, tpre);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(tok);
+  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * s_.n_layers, st_));
+  CK(cudaStreamSynchronize(st_));
+  return TD_OK;
+}
+
+// ------------------------------------------------------------------ factory
+td_status Engine::create(const td_model_shape& s, int n_stages, const td_options& o, Engine** out,
+                         std::string* err) {
+  auto* e = new CudaEngine();
+  td_status st = e->init(s, n_stages, o);
+  if (st != TD_OK) {
+    *err = e->error;
+    delete e;
+    return st;
+  }
+  *out = e;
+  return TD_OK;
+}
+
+}  // namespace tdp

@@ -1,0 +1,79 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (all async on `st`).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tdp {
+
+typedef __nv_bfloat16 bf16;
+
+// ---- weight init (F9 counter-based recipe), physical layouts -------------
+enum InitMap { kMapIdentity = 0, kMapQKV = 1, kMapGateUp = 2 };
+enum InitKind { kInitProj = 0, kInitNorm = 1, kInitEmbed = 2 };
+struct InitSpec {
+  int map;            // InitMap
+  int kind;           // InitKind
+  int rows, cols;     // physical [rows, cols]
+  int tid0, tid1, tid2;   // tensor ids (QKV: q,k,v; gate/up: g,u)
+  int H, Hkv, hd;     // for kMapQKV
+  float scale;        // sqrt_f32(3/fan_in) for projections
+};
+void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st);
+
+// ---- embedding / norms / sampling -----------------------------------------
+void launch_embed(const int32_t* arena, const int32_t* tok_idx, const bf16* E, float* x, int T, int d,
+                  cudaStream_t st);
+// out[i] = bf16(RMSNorm(x[rows ? rows[i] : i]) * g)
+void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* rows, int n, int d, float eps,
+                    cudaStream_t st);
+// tokens: arena[outpos[i]] = argmax_j logits[i][j] (lowest index on ties)
+void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int32_t* outpos, cudaStream_t st);
+
+// ---- GEMM: C[M,N] = A[M,K] . W[N,K]^T, bf16 in, fp32 accumulate ----------
+enum GemmEpi { kEpiF32 = 0, kEpiResid = 1, kEpiSwiGLU = 2, kEpiQKV = 3, kEpiBF16 = 4 };
+struct EpiParams {
+  int mode;
+  float* out_f32;        // kEpiF32: [M, ldo]; kEpiResid: x [M, ldo] (+=)
+  bf16* out_bf16;        // kEpiSwiGLU: h [M, N/2]; kEpiQKV: q [M, H*hd]; kEpiBF16
+  int ldo;
+  // QKV epilogue (RoPE + paged KV write)
+  bf16* kcache;          // this layer's pool base: [nblk][2][Hkv][16][hd]
+  const int32_t* pos;    // [M]
+  const int32_t* slot;   // [M] physical token slot = blk*16 + off
+  const float* rope_cs;  // [max_pos][hd/2][2] (cos, sin)
+  int H, Hkv, hd;
+};
+void launch_gemm(const bf16* A, const bf16* W, int M, int N, int K, const EpiParams& ep, cudaStream_t st);
+
+// ---- attention --------------------------------------------------------------
+// Decode: one query token per sequence; q [n, H*hd] (physical RoPE-pair order),
+// paged K/V via block tables; o [n, H*hd] bf16.  Split-KV over fixed 512-token
+// chunks (batch-invariant), partial (m, l, acc) merged in a fixed order.
+struct DecodeAttnParams {
+  const bf16* q;
+  const bf16* kv;        // layer pool base
+  const int32_t* ctx;    // [n] context length incl. the new token
+  const int32_t* bt;     // [n, maxblk]
+  int maxblk;
+  bf16* o;
+  float* part;           // [n, H, max_splits, hd + 2] workspace
+  int max_splits;
+  int n, H, Hkv, hd;
+};
+void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
+
+// Prefill: varlen causal over each sequence's own (paged) K/V.
+struct PrefillAttnParams {
+  const bf16* q;         // [T, H*hd]
+  const bf16* kv;
+  const int32_t* tok_seq;   // [T] sequence index
+  const int32_t* tok_pos;   // [T] absolute position
+  const int32_t* bt;        // [n, maxblk]
+  int maxblk;
+  bf16* o;                  // [T, H*hd]
+  int T, H, Hkv, hd;
+};
+void launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t st);
+
+}  // namespace tdp

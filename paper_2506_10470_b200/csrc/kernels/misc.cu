@@ -1,0 +1,171 @@
+// misc.cu -- weight init (F9 recipe), embedding gather, RMSNorm, argmax.
+//
+// Memory-bound helpers: vectorised 16-byte loads, one CTA per row, grid sized
+// by the row count.  RMSNorm(x) = x / sqrt(mean(x^2) + eps) * g (Llama
+// pre-norm) in fp32 from the fp32 residual.
+#include <float.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tdp {
+
+// splitmix64 finaliser (counter-based; both sides implement it independently)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_kernel(bf16* __restrict__ dst, InitSpec s, uint64_t seed) {
+  const int64_t total = (int64_t)s.rows * s.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(e / s.cols);
+    const int c = (int)(e % s.cols);
+    int tid = s.tid0, row = p;
+    if (s.map == kMapQKV) {
+      // physical rows: q heads, k heads, v heads; q/k rows interleave the
+      // rotate-half pairs (i, i + hd/2) as (2i, 2i+1) so RoPE is an in-thread pair
+      const int qrows = s.H * s.hd, krows = s.Hkv * s.hd;
+      int base = 0;
+      if (p < qrows) { tid = s.tid0; base = 0; }
+      else if (p < qrows + krows) { tid = s.tid1; base = qrows; }
+      else { tid = s.tid2; base = qrows + krows; }
+      const int lp = p - base;
+      if (tid == s.tid2) {
+        row = lp;
+      } else {
+        const int h = lp / s.hd, j = lp % s.hd;
+        const int i = (j & 1) ? (s.hd / 2 + j / 2) : (j / 2);
+        row = h * s.hd + i;
+      }
+    } else if (s.map == kMapGateUp) {
+      tid = (p & 1) ? s.tid1 : s.tid0;
+      row = p >> 1;
+    }
+    const uint64_t idx = (uint64_t)row * (uint64_t)s.cols + (uint64_t)c;
+    const uint64_t h = splitmix64(seed ^ ((uint64_t)tid << 40) ^ idx);
+    const float u = __fmul_rn((float)(h >> 40), 5.9604644775390625e-08f);   // * 2^-24, exact
+    const float v = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);                      // exact
+    float w;
+    if (s.kind == kInitProj) w = __fmul_rn(s.scale, v);
+    else if (s.kind == kInitNorm) w = __fadd_rn(1.0f, __fmul_rn(0.1f, v));
+    else w = v;
+    dst[e] = __float2bfloat16_rn(w);
+  }
+}
+
+void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st) {
+  const int64_t total = (int64_t)s.rows * s.cols;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  init_kernel<<<blocks, 256, 0, st>>>(dst, s, seed);
+}
+
+// ----------------------------------------------------------------- embedding
+__global__ void embed_kernel(const int32_t* __restrict__ arena, const int32_t* __restrict__ tok_idx,
+                             const bf16* __restrict__ E, float* __restrict__ x, int d) {
+  const int t = blockIdx.x;
+  const int tok = arena[tok_idx[t]];
+  const uint4* src = reinterpret_cast<const uint4*>(E + (int64_t)tok * d);
+  float4* dst = reinterpret_cast<float4*>(x + (int64_t)t * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    float f[8];
+    bf16x8_to_f32(src[i], f);
+    dst[2 * i] = make_float4(f[0], f[1], f[2], f[3]);
+    dst[2 * i + 1] = make_float4(f[4], f[5], f[6], f[7]);
+  }
+}
+
+void launch_embed(const int32_t* arena, const int32_t* tok_idx, const bf16* E, float* x, int T, int d,
+                  cudaStream_t st) {
+  if (T <= 0) return;
+  embed_kernel<<<T, 128, 0, st>>>(arena, tok_idx, E, x, d);
+}
+
+// ------------------------------------------------------------------- RMSNorm
+template <int NT>
+__global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
+                                                     bf16* __restrict__ out, const int32_t* __restrict__ rows,
+                                                     int d, float eps) {
+  const int i = blockIdx.x;
+  const int r = rows ? rows[i] : i;
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)r * d);
+  __shared__ float red[NT / 32];
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d / 4; j += NT) {
+    float4 v = xr[j];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < NT / 32 ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)d + eps);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g);
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)i * d);
+  for (int j = threadIdx.x; j < d / 4; j += NT) {
+    float4 v = xr[j];
+    float2 ga = __bfloat1622float2(g2[2 * j]);
+    float2 gb = __bfloat1622float2(g2[2 * j + 1]);
+    uint2 pk;
+    pk.x = pack_bf16x2(v.x * inv * ga.x, v.y * inv * ga.y);
+    pk.y = pack_bf16x2(v.z * inv * gb.x, v.w * inv * gb.y);
+    o[j] = pk;
+  }
+}
+
+void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* rows, int n, int d, float eps,
+                    cudaStream_t st) {
+  if (n <= 0) return;
+  rmsnorm_kernel<256><<<n, 256, 0, st>>>(x, g, out, rows, d, eps);
+}
+
+// -------------------------------------------------------------------- argmax
+__global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ arena,
+                              const int32_t* __restrict__ outpos) {
+  const int i = blockIdx.x;
+  const float* l = logits + (int64_t)i * V;
+  float best = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    const float v = l[j];
+    if (v > best) { best = v; bi = j; }   // strided scan: first max within a thread
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) { sb[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    best = threadIdx.x < nw ? sb[threadIdx.x] : -FLT_MAX;
+    bi = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (threadIdx.x == 0) arena[outpos[i]] = bi;
+  }
+}
+
+void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int32_t* outpos, cudaStream_t st) {
+  if (n <= 0) return;
+  argmax_kernel<<<n, 256, 0, st>>>(logits, V, arena, outpos);
+}
+
+}  // namespace tdp
