@@ -1,0 +1,288 @@
+#!/usr/bin/env python
+"""TD-Pipe hot-path benchmark (contract: one JSON line on rank 0).
+
+Step = one pass of the whole hot path over one batch of synthetic input: the
+complete offline job of BASELINE.json config[1] at N=1 -- Llama-2-7B-shaped
+random-init weights (all 32 layers), 256 ShareGPT-length requests with
+bucket-predicted output lengths, run to completion by the TD-Pipe controller
+(prefill phases + decode phases).  Metric: generated
+tokens/s (BASELINE.json "metric"), plus bubble %, roofline fractions.
+
+  value  generated tokens / device time of td_run (CUDA events on the library's
+         stream), prompts already resident in HBM (td_upload before timing)
+  e2e    same metric through the C ABI from HOST buffers: td_submit + td_upload
+         (H2D) + td_run + td_get_outputs (D2H) inside the timed region
+
+--impl reference times the oracle (oracle/, numpy fp64) on the host cores on a
+bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from workload import SHAPES, config_workload  # noqa: E402
+
+METRIC = "generated tokens/s (8×B200 pipeline) + bubble %, HBM/TC roofline fraction"
+UNIT = "tokens/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], tc=d["bf16_tflops"], tc_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, tc=1590.0, tc_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------- oracle arm
+def oracle_sample(shape_name="llama2_7b", layers=2, n_tokens=2, seed=2):
+    """The oracle as it stands, on a bounded sample of the C2 workload: greedy
+    decode of `n_tokens` tokens of request 0 through `layers` of the 32 layers,
+    scaled to the full depth.  Returns (tokens/s, seconds, description)."""
+    from oracle import forward as F
+    from oracle.weights import OracleWeights
+    full = SHAPES[shape_name]
+    shape = full.with_layers(layers)
+    wl = config_workload("C2")
+    prompt = wl.requests[0].prompt
+    W = OracleWeights(shape)
+    W.embed(); W.lm_head(); W.final_norm()
+    for l in range(layers):
+        W.layer(l)
+    t0 = time.perf_counter()
+    F.greedy_generate(W, prompt, n_tokens)
+    dt = time.perf_counter() - t0
+    scaled = dt * full.n_layers / layers
+    desc = (f"oracle greedy decode of {n_tokens} tokens of C2 request 0 (prompt {len(prompt)}) through "
+            f"{layers}/{full.n_layers} Llama-2-7B-shaped layers, fp64 numpy, time scaled x{full.n_layers / layers:g}")
+    return n_tokens / scaled, dt, desc
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        v, dt, desc = oracle_sample()
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: Llama-2-7B-shaped random-init, 1 GPU, 256 ShareGPT-length requests",
+                       "parallelism": f"pp{args.gpus}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- our arm
+def run_ours(args):
+    import paper_2506_10470_b200 as tp
+    from paper_2506_10470_b200 import TDPipe
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        return run_ours_multiprocess(args, world, rank)
+    peaks = load_peaks()
+    shape = SHAPES[args.model]
+    wl = config_workload(args.config)
+    n_req = len(wl.requests)
+    policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
+              "ppsb_alt": tp.TD_POLICY_PPSB_ALT}[args.policy]
+    t = TDPipe(shape, args.stages, device=0, policy=policy, eq2_bubble_scale=args.sigma)
+    info = t.td_info()
+    # frozen profile table for Eq.1/Eq.2, measured once, untimed
+    L = np.array([len(r.prompt) for r in wl.requests])
+    P = np.array([r.predicted_len for r in wl.requests])
+    ctx_rep = int(L.sum() // n_req + (P.sum() // n_req) // 2)
+    prof = os.path.join(tempfile.gettempdir(), f"tdpipe_profile_{os.getpid()}.csv")
+    t0 = time.perf_counter()
+    t.td_profile(prof, min(1024, max(n_req, 1)), 2048, ctx_rep)
+    prof_s = time.perf_counter() - t0
+
+    def one_step():
+        t.td_reset()
+        t.submit_workload(wl)
+        t.td_upload()
+        return t.td_run()
+
+    t.td_set_timing(False)
+    for _ in range(args.warmup):
+        one_step()
+    sampler = ClockSampler(0)
+    sampler.start()
+    stats = []
+    t.td_set_timing(not args.no_timing)        # per-kernel CUDA events over the timed region
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        stats.append(one_step())
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    gen = sum(s["generated_tokens"] for s in stats)
+    dev_s = sum(s["makespan_ns"] for s in stats) / 1e9
+    value = gen / dev_s
+    # roofline of the dominant kernel class over the timed region
+    kern = {}
+    if not args.no_timing:
+        for name in ["decode_attn", "prefill_attn", "gemm_qkv", "gemm_o", "gemm_gu", "gemm_down", "lm_head"]:
+            kern[name] = t.td_get_timing(name)   # accumulated over the K timed steps
+    # e2e: host buffers through the public API, H2D + D2H inside the timed region
+    e2e_vals = []
+    h2d = d2h = 0
+    t.td_set_timing(False)
+    for _ in range(max(1, min(args.steps, 2))):
+        t.td_reset()
+        s0 = time.perf_counter()
+        t.submit_workload(wl)
+        t.td_upload()
+        st = t.td_run()
+        out, n = t.td_get_outputs(n_req, int(max(r.max_new_tokens for r in wl.requests)))
+        e2e_vals.append(st["generated_tokens"] / (time.perf_counter() - s0))
+        h2d = int(sum(len(r.prompt) + r.max_new_tokens + 1 for r in wl.requests) * 4 + st["h2d_bytes"])
+        d2h = int(sum(len(r.prompt) + r.max_new_tokens + 1 for r in wl.requests) * 4)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.config}: Llama-2-7B-shaped random-init (32 layers), {n_req} ShareGPT-length "
+                               f"requests, bucket-predicted lengths, {args.stages}-stage TD-Pipe ({args.policy})",
+                   "model": shape.name, "n_requests": n_req, "global_batch": n_req,
+                   "parallelism": f"pp{args.stages}", "l2": "inputs larger than L2 (13.5 GB weights + KV per step)",
+                   "kv_blocks": info["kv_blocks"], "profile_s": round(prof_s, 2)},
+        "bubble_pct": 100.0 * statistics.mean(s["bubble_frac"] for s in stats) if not args.no_timing else None,
+        "total_tokens_per_s": sum(s["generated_tokens"] + s["prompt_tokens"] for s in stats) / dev_s,
+        "wall_tokens_per_s": gen / wall,
+        "gpu_launches": int(sum(s["gpu_launches"] for s in stats)),
+        "sched": {k: stats[-1][k] for k in ["n_microbatches", "n_prefill_mb", "n_decode_mb", "n_p2d", "n_d2p",
+                                            "n_stolen", "n_evicted", "prompt_tokens", "generated_tokens"]},
+        "clocks": clocks,
+        "e2e": {"value": statistics.mean(e2e_vals), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+    }
+    if kern:
+        tot_ms = sum(k["ms"] for k in kern.values())
+        dom = max(kern, key=lambda k: kern[k]["ms"])
+        share = {k: round(v["ms"] / tot_ms, 4) for k, v in kern.items() if tot_ms > 0}
+        rl = {}
+        for k, v in kern.items():
+            if v["ms"] <= 0:
+                continue
+            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            tfs = v["flops"] / (v["ms"] * 1e-3) / 1e12
+            rl[k] = {"launches": v["launches"], "ms": round(v["ms"], 3), "GB/s": round(gbs, 1),
+                     "TFLOP/s": round(tfs, 1), "hbm_frac": round(gbs / peaks["hbm"], 4),
+                     "tc_frac": round(tfs / peaks["tc_sus"], 4)}
+        d = kern[dom]
+        if dom in ("decode_attn",) or (d["flops"] > 0 and d["bytes"] / max(d["flops"], 1) > 1 / 250):
+            ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+            line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"],
+                                "unit": "GB/s", "frac": round(ach / peaks["hbm"], 4), "traffic": None,
+                                "peak_src": peaks["src"]}
+        else:
+            ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
+            line["roofline"] = {"kernel": dom, "bound": "tensor", "achieved": round(ach, 1), "peak": peaks["tc_sus"],
+                                "unit": "TFLOP/s", "frac": round(ach / peaks["tc_sus"], 4), "traffic": None,
+                                "peak_src": peaks["src"] + " sustained"}
+        line["kernels"] = rl
+        line["kernel_share"] = share
+    if not args.no_cpu_baseline:
+        v, dt, desc = oracle_sample()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc,
+                                "seconds": round(dt, 2)}
+    t.close()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours_multiprocess(args, world, rank):
+    raise SystemExit("multi-process pipeline: see bench_mp (not built in this revision)")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--model", default="llama2_7b")
+    ap.add_argument("--stages", type=int, default=1)
+    ap.add_argument("--policy", default="tdpipe", choices=["tdpipe", "ppsb_prio", "ppsb_alt"])
+    ap.add_argument("--sigma", type=int, default=1)
+    ap.add_argument("--no-timing", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -82,7 +82,10 @@ class CudaEngine : public Engine {
   td_status kv_reset() override;
   td_status profile(int b_max, int k_max, int ctx_len, std::vector<int64_t>* tdec,
                     std::vector<int64_t>* tpre) override;
-  void set_timing(bool on) override { timing_ = on; }
+  void set_timing(bool on) override {
+    if (on && !timing_) timing_acc_.clear();   // a new timed region starts
+    timing_ = on;
+  }
   bool get_timing(const std::string& name, KernelTiming* t) override;
 
  private:
@@ -548,7 +551,6 @@ td_status CudaEngine::begin_run(const std::vector<HostReq>& reqs, bool record_lo
   launches_ = 0;
   timed_.clear();
   ev_used_ = 0;
-  timing_acc_.clear();
   started_ = false;
   for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
   return TD_OK;
