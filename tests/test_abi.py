@@ -14,7 +14,7 @@ HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 
 def declared():
     src = open(HDR).read()
-    return sorted(set(re.findall(r"\b(td_[a-z_0-9]+)\s*\(", src)))
+    return sorted(set(re.findall(r"^(?:td_status|void|const char\*|int64_t)\s+(td_\w+)\(", src, re.M)))
 
 
 def test_every_declared_symbol_is_exported():
