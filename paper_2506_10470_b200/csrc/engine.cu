@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -29,6 +30,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "kernels/gemm_tc.h"
 #include "kernels/kernels.h"
 
 namespace tdp {
@@ -46,6 +48,12 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct LayerW {
   bf16 *wqkv, *wo, *wgu, *wd, *g1, *g2;
+  TcOperand tqkv, to, tgu, td;   // TMA descriptors (box 64 x 128)
+};
+
+// X operands of the tcgen05 GEMM: one TMA descriptor per token-tile width.
+struct XOps {
+  TcOperand by_bn[4];
 };
 
 // Per-micro-batch metadata (host-built, one H2D copy): int32 arrays.
@@ -96,8 +104,11 @@ class CudaEngine : public Engine {
                   const std::vector<const std::vector<int32_t>*>& blocks, const int32_t* bt_flat, int bt_stride);
   td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena);
   td_status run_microbatch(const Meta& M, const int32_t* dmeta, int32_t* arena);
-  void tbegin(int cls);
-  void tend(int cls, double bytes, double flops);
+  td_status make_x_ops();
+  void gemm(const bf16* A, const XOps& xo, const LayerW* lw, const TcOperand& W, const bf16* Wraw, int T, int N,
+            int K, const EpiParams& ep, bool decode);
+  int tbegin(int cls);
+  void tend(int idx, double bytes, double flops);
   int ring_acquire();
 
   td_model_shape s_{};
@@ -115,6 +126,11 @@ class CudaEngine : public Engine {
   bf16* kv_ = nullptr;
   int64_t C_ = 0, kv_block_bytes_layer_ = 0;
   float* rope_ = nullptr;
+  TcOperand tlm_;
+  XOps xa_, xo_, xh_;
+  float* ws_ = nullptr;
+  int64_t ws_cap_ = 0;
+  bool use_mma_ = false;
   // work
   int64_t capT_ = 0, capN_ = 0, capBlk_ = 0;
   float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
@@ -229,6 +245,16 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   InitSpec gf{kMapIdentity, kInitNorm, 1, d_, 1 + 9 * L, 0, 0, 0, 0, 0, 0.f};
   launch_init(gf_, gf, o.weight_seed, st_);
   CK(cudaGetLastError());
+  use_mma_ = getenv("TDPIPE_GEMM") && std::string(getenv("TDPIPE_GEMM")) == "mma";
+  for (int i = 0; i < L; ++i) {
+    LayerW& w = L_[i];
+    if (!make_tc_operand(&w.tqkv, w.wqkv, (int)nqkv, d_, 128) || !make_tc_operand(&w.to, w.wo, d_, H_ * hd_, 128) ||
+        !make_tc_operand(&w.tgu, w.wgu, 2 * F_, d_, 128) || !make_tc_operand(&w.td, w.wd, d_, F_, 128)) {
+      error = "cuTensorMapEncodeTiled failed (weights)";
+      return TD_ECUDA;
+    }
+  }
+  if (!make_tc_operand(&tlm_, Wlm_, V_, d_, 128)) { error = "cuTensorMapEncodeTiled failed (lm)"; return TD_ECUDA; }
   // ---- RoPE table [max_seq_len][hd/2] (cos, sin), from double
   {
     const int P = s.max_seq_len, half = hd_ / 2;
@@ -279,6 +305,7 @@ void CudaEngine::release() {
   cudaFree(ob_);
   cudaFree(h_);
   cudaFree(arena_);
+  cudaFree(ws_);
   for (int i = 0; i < kRing; ++i) {
     if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
     cudaFree(dmeta_[i]);
@@ -323,7 +350,48 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   capT_ = T;
   capN_ = n;
   capBlk_ = maxblk;
+  // split-K workspace (decode GEMMs with few output tiles): 4 x 512 x max(Nf)
+  const int64_t wneed = 4LL * 512 * std::max<int64_t>((int64_t)(H_ + 2 * Hkv_) * hd_, d_);
+  if (wneed > ws_cap_) {
+    cudaFree(ws_);
+    CK(cudaMalloc(&ws_, wneed * 4));
+    ws_cap_ = wneed;
+  }
+  return make_x_ops();
+}
+
+td_status CudaEngine::make_x_ops() {
+  for (int i = 0; i < 4; ++i) {
+    const int box = 32 << i;
+    if (!make_tc_operand(&xa_.by_bn[i], a_, (int)capT_, d_, box) ||
+        !make_tc_operand(&xo_.by_bn[i], ob_, (int)capT_, H_ * hd_, box) ||
+        !make_tc_operand(&xh_.by_bn[i], h_, (int)capT_, F_, box)) {
+      error = "cuTensorMapEncodeTiled failed (activations)";
+      return TD_ECUDA;
+    }
+  }
   return TD_OK;
+}
+
+// Dense weight GEMM dispatch: tcgen05 kernel (default) or the mma.sync
+// baseline (TDPIPE_GEMM=mma, A/B comparisons only).  Split-K only for decode
+// micro-batches, with a count fixed by (N, K): batch-invariant.
+void CudaEngine::gemm(const bf16* A, const XOps& xo, const LayerW* lw, const TcOperand& W, const bf16* Wraw, int T,
+                      int N, int K, const EpiParams& ep, bool decode) {
+  (void)lw;
+  if (use_mma_) {
+    launch_gemm(A, Wraw, T, N, K, ep, st_);
+    return;
+  }
+  int splits = 1;
+  if (decode && T <= 512) {
+    const int tiles = (N + 127) / 128;
+    splits = std::max(1, std::min(4, 148 / tiles));
+    while (splits > 1 && (K / 64) / splits < 8) --splits;
+    if ((int64_t)splits * T * N > ws_cap_) splits = 1;
+  }
+  launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, st_);
+  if (splits > 1) launches_++;
 }
 
 // -------------------------------------------------------------------- ring
@@ -384,8 +452,8 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
 }
 
 // ------------------------------------------------------------------ timing
-void CudaEngine::tbegin(int cls) {
-  if (!timing_) return;
+int CudaEngine::tbegin(int cls) {
+  if (!timing_) return -1;
   if (ev_used_ + 2 > ev_pool_.size()) {
     for (int i = 0; i < 256; ++i) {
       cudaEvent_t e;
@@ -400,11 +468,11 @@ void CudaEngine::tbegin(int cls) {
   tl.bytes = tl.flops = 0;
   cudaEventRecord(tl.a, st_);
   timed_.push_back(tl);
+  return (int)timed_.size() - 1;
 }
-void CudaEngine::tend(int cls, double bytes, double flops) {
-  if (!timing_) return;
-  TimedLaunch& tl = timed_.back();
-  (void)cls;
+void CudaEngine::tend(int idx, double bytes, double flops) {
+  if (!timing_ || idx < 0) return;
+  TimedLaunch& tl = timed_[idx];
   tl.bytes = bytes;
   tl.flops = flops;
   cudaEventRecord(tl.b, st_);
@@ -440,44 +508,44 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ep.H = H_;
     ep.Hkv = Hkv_;
     ep.hd = hd_;
-    tbegin(cQKV);
-    launch_gemm(a_, w.wqkv, T, nqkv, d_, ep, st_);
-    tend(cQKV, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
+    const int iq = tbegin(cQKV);
+    gemm(a_, xa_, &w, w.tqkv, w.wqkv, T, nqkv, d_, ep, !M.prefill);
+    tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.prefill) {
       PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_};
-      tbegin(cPreAttn);
+      const int ip = tbegin(cPreAttn);
       launch_prefill_attn(pp, st_);
-      tend(cPreAttn, 0, 0);
+      tend(ip, 0, 0);
       launches_++;
     } else {
       const int ms = (int)cdiv(M.max_ctx, 512);
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_};
-      tbegin(cDecAttn);
+      const int ida = tbegin(cDecAttn);
       launch_decode_attn(dp, st_);
-      tend(cDecAttn, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
+      tend(ida, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
       launches_ += ms > 1 ? 2 : 1;
     }
     EpiParams eo{};
     eo.mode = kEpiResid;
     eo.out_f32 = x_;
     eo.ldo = d_;
-    tbegin(cO);
-    launch_gemm(ob_, w.wo, T, d_, H_ * hd_, eo, st_);
-    tend(cO, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
+    const int io = tbegin(cO);
+    gemm(ob_, xo_, &w, w.to, w.wo, T, d_, H_ * hd_, eo, !M.prefill);
+    tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
     launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
     EpiParams eg{};
     eg.mode = kEpiSwiGLU;
     eg.out_bf16 = h_;
-    tbegin(cGU);
-    launch_gemm(a_, w.wgu, T, 2 * F_, d_, eg, st_);
-    tend(cGU, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
+    const int ig = tbegin(cGU);
+    gemm(a_, xa_, &w, w.tgu, w.wgu, T, 2 * F_, d_, eg, !M.prefill);
+    tend(ig, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
     EpiParams ed{};
     ed.mode = kEpiResid;
     ed.out_f32 = x_;
     ed.ldo = d_;
-    tbegin(cDown);
-    launch_gemm(h_, w.wd, T, d_, F_, ed, st_);
-    tend(cDown, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
+    const int idn = tbegin(cDown);
+    gemm(h_, xh_, &w, w.td, w.wd, T, d_, F_, ed, !M.prefill);
+    tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     launches_ += 6;
   }
   if (stage == S_ - 1) {
@@ -486,9 +554,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     el.mode = kEpiF32;
     el.out_f32 = logits_;
     el.ldo = V_;
-    tbegin(cLM);
-    launch_gemm(a_, Wlm_, n, V_, d_, el, st_);
-    tend(cLM, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
+    const int il = tbegin(cLM);
+    gemm(a_, xa_, nullptr, tlm_, Wlm_, n, V_, d_, el, !M.prefill);
+    tend(il, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
     launches_ += 2;
     if (arena) {
       launch_argmax(logits_, n, V_, arena, dm + M.o_outpos, st_);
@@ -500,14 +568,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
 
 td_status CudaEngine::run_microbatch(const Meta& M, const int32_t* dm, int32_t* arena) {
   for (int s = 0; s < S_; ++s) {
-    cudaEvent_t a = nullptr, b = nullptr;
-    if (timing_) {
-      tbegin(cStage);
-    }
+    const int is = tbegin(cStage);
     if (td_status e = run_stage(s, M, dm, arena)) return e;
-    if (timing_) tend(cStage, 0, 0);
-    (void)a;
-    (void)b;
+    tend(is, 0, 0);
   }
   return TD_OK;
 }

@@ -1,0 +1,291 @@
+// gemm_tc.cu -- tcgen05 / TMEM / TMA GEMM for sm_100a (the dense weight GEMMs).
+//
+//   out[t][f] = sum_k X[t][k] * W[f][k]      X: activations [T, K], W: weights [Nf, K]
+//
+// Swap-AB: the weight tile is the MMA M operand (128 output features per CTA,
+// TMEM lane = feature) and the token tile is the N operand (BN <= 256 tokens,
+// TMEM column = token).  Decode batches (T <= 256) therefore need exactly one
+// N tile and every weight byte is streamed from HBM once; prefill walks T in
+// BN = 256 tiles.  Operands are staged by TMA (128B swizzle, K-major) into a
+// STAGES-deep smem ring; one elected thread issues tcgen05.mma (kind::f16,
+// bf16 in, fp32 accumulate in TMEM); 4 epilogue warps tcgen05.ld the
+// accumulator and apply the fused epilogue (epilogue.cuh), where a feature pair
+// (2i, 2i+1) sits in adjacent lanes (RoPE pair / gate-up pair via one shfl).
+//
+// Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
+// w2..w5 epilogue (TMEM lane quarter = warp % 4).
+//
+// Split-K (decode only, count fixed per (Nf, K) so results do not depend on
+// the batch): partial fp32 tiles go to a workspace, reduced in split order by
+// splitk_reduce_kernel which applies the same epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "kernels.h"
+#include "gemm_tc.h"
+
+namespace tdp {
+
+namespace {
+constexpr int BK = 64;            // 64 bf16 = 128 B rows = one 128B swizzle atom
+constexpr int A_BYTES = 128 * BK * 2;
+
+TDP_DEV void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+TDP_DEV void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t a = smem_u32(b);
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+TDP_DEV void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+TDP_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+TDP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+TDP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+TDP_DEV void umma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+TDP_DEV void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// K-major, 128B-swizzled canonical layout: 8-row x 128 B atoms, SBO = 1024 B.
+TDP_DEV uint64_t smem_desc_sw128(const void* p) {
+  const uint64_t a = smem_u32(p);
+  uint64_t d = 0;
+  d |= (a >> 4) & 0x3FFFull;            // start address
+  d |= (uint64_t)1 << 16;               // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;     // SBO
+  d |= (uint64_t)1 << 46;               // sm100 descriptor version
+  d |= (uint64_t)2 << 61;               // SWIZZLE_128B
+  return d;
+}
+TDP_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Nf, int T,
+               int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws) {
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accf = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 128;
+  const int n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = min(kb_per_split, kb_total - kb0);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(sa, &tmW, (kb0 + i) * BK, m0, &full[s]);
+        tma_load_2d(sa + A_BYTES, &tmX, (kb0 + i) * BK, n0, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=BN
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        const uint64_t ad = smem_desc_sw128(sa);
+        const uint64_t bd = smem_desc_sw128(sa + A_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)   // advance 16 elements = 32 B inside the swizzle atom
+          umma_f16(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(accf);
+    }
+  } else {
+    // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    mbar_wait(accf, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int f = m0 + q * 32 + lane;            // this lane's output feature
+    const bool even = (lane & 1) == 0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
+      if (ws) {
+        // split-K partial: ws[split][t][f]
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int t = n0 + c + j;
+          if (t < T && f < Nf) ws[((int64_t)blockIdx.z * T + t) * Nf + f] = __uint_as_float(r[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float v = __uint_as_float(r[j]);
+          const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
+          const int t = n0 + c + j;
+          if (even && t < T) epilogue_pair(ep, T, Nf, t, f, v, vp);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
+  const int64_t pairs = (int64_t)T * (Nf >> 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / (Nf >> 1));
+    const int f = (int)(i % (Nf >> 1)) * 2;
+    float v0 = 0.f, v1 = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float2 p = *reinterpret_cast<const float2*>(ws + ((int64_t)s * T + t) * Nf + f);
+      v0 += p.x;
+      v1 += p.y;
+    }
+    epilogue_pair(ep, T, Nf, t, f, v0, v1);
+  }
+}
+
+template <int BN, int STAGES>
+constexpr int smem_bytes() {
+  return STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
+}
+
+template <int BN, int STAGES>
+void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, int splits, float* ws,
+               cudaStream_t st) {
+  auto kern = gemm_tc_kernel<BN, STAGES>;
+  static bool attr = false;
+  constexpr int sm = smem_bytes<BN, STAGES>();
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    attr = true;
+  }
+  const int kb_total = W.K / BK;
+  const int kps = (kb_total + splits - 1) / splits;
+  const int nsplit = (kb_total + kps - 1) / kps;
+  dim3 grid((W.rows + 127) / 128, (T + BN - 1) / BN, nsplit);
+  kern<<<grid, 192, sm, st>>>(W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr);
+  if (nsplit > 1) {
+    const int64_t pairs = (int64_t)T * (W.rows / 2);
+    int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, nsplit, T, W.rows, ep);
+  }
+}
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_tc_operand(TcOperand* op, const bf16* base, int rows, int K, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  op->base = base;
+  op->rows = rows;
+  op->K = K;
+  op->box_rows = box_rows;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&op->map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int tc_bn_for(int T) { return T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
+
+void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
+                    cudaStream_t st) {
+  if (T <= 0) return;
+  switch (tc_bn_for(T)) {
+    case 32: launch_bn<32, 8>(W, Xby_bn[0], T, ep, splits, ws, st); break;
+    case 64: launch_bn<64, 8>(W, Xby_bn[1], T, ep, splits, ws, st); break;
+    case 128: launch_bn<128, 6>(W, Xby_bn[2], T, ep, splits, ws, st); break;
+    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, st); break;
+  }
+}
+
+}  // namespace tdp

@@ -1,0 +1,25 @@
+// gemm_tc.h -- host interface of the tcgen05/TMA GEMM (gemm_tc.cu).
+#pragma once
+#include <cuda.h>
+
+#include "kernels.h"
+
+namespace tdp {
+
+// A K-major bf16 matrix [rows, K] with its TMA descriptor (box = 64 x box_rows,
+// 128B swizzle).  Weights use box_rows = 128; activation buffers one operand
+// per token-tile width BN in {32, 64, 128, 256}.
+struct TcOperand {
+  CUtensorMap map;
+  const bf16* base = nullptr;
+  int rows = 0, K = 0, box_rows = 0;
+};
+
+bool make_tc_operand(TcOperand* op, const bf16* base, int rows, int K, int box_rows);
+int tc_bn_for(int T);
+// out = X[T, K] . W[Nf, K]^T with epilogue ep.  Xby_bn[i] = X described with
+// box rows 32 << i.  splits > 1: split-K through workspace ws [splits][T][Nf].
+void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
+                    cudaStream_t st);
+
+}  // namespace tdp

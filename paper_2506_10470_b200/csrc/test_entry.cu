@@ -1,0 +1,51 @@
+// test_entry.cu -- td_test_gemm: kernel-level unit-test entry point (testing only).
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../../include/tdpipe.h"
+#include "kernels/gemm_tc.h"
+#include "kernels/kernels.h"
+
+using namespace tdp;
+
+extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N,
+                                  int32_t K, int32_t impl, int32_t splits, float* out) {
+  if (!A || !W || !out || T < 1 || N < 2 || (N & 1) || K < 64 || K % 64) return TD_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
+  bf16 *dA = nullptr, *dW = nullptr;
+  float *dO = nullptr, *ws = nullptr;
+  const int Tcap = ((T + 255) / 256) * 256;
+  td_status st = TD_OK;
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  if (cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dW, (size_t)N * K * 2) ||
+      cudaMalloc(&dO, (size_t)T * N * 4) || cudaMalloc(&ws, (size_t)std::max(splits, 1) * T * N * 4)) {
+    st = TD_ENOMEM;
+  } else {
+    cudaMemset(dA, 0, (size_t)Tcap * K * 2);
+    cudaMemcpy(dA, A, (size_t)T * K * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dW, W, (size_t)N * K * 2, cudaMemcpyHostToDevice);
+    EpiParams ep{};
+    ep.mode = kEpiF32;
+    ep.out_f32 = dO;
+    ep.ldo = N;
+    if (impl == 1) {
+      launch_gemm(dA, dW, T, N, K, ep, s);
+    } else {
+      TcOperand w, x[4];
+      bool ok = make_tc_operand(&w, dW, N, K, 128);
+      for (int i = 0; i < 4; ++i) ok = ok && make_tc_operand(&x[i], dA, Tcap, K, 32 << i);
+      if (!ok) st = TD_ECUDA;
+      else launch_gemm_tc(w, x, T, ep, splits, ws, s);
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
+    if (st == TD_OK) cudaMemcpy(out, dO, (size_t)T * N * 4, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dA);
+  cudaFree(dW);
+  cudaFree(dO);
+  cudaFree(ws);
+  cudaStreamDestroy(s);
+  return st;
+}

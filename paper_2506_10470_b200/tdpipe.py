@@ -62,7 +62,7 @@ class td_batch(C.Structure):
 EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td_submit", "td_upload",
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
-           "td_get_timing", "td_nccl_ids"]
+           "td_get_timing", "td_nccl_ids", "td_test_gemm"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -95,6 +95,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_get_timing.argtypes = [C.c_void_p, C.c_char_p, P(C.c_int64), P(C.c_double), P(C.c_double),
                                   P(C.c_double)]
     lib.td_nccl_ids.argtypes = [C.c_void_p]
+    lib.td_test_gemm.argtypes = [C.c_int32, P(C.c_uint16), P(C.c_uint16), C.c_int32, C.c_int32, C.c_int32,
+                                 C.c_int32, C.c_int32, P(C.c_float)]
     for f in EXPORTS:
         if f not in ("td_default_options", "td_destroy", "td_last_error", "td_submit"):
             getattr(lib, f).restype = C.c_int32
@@ -270,3 +272,17 @@ def td_nccl_ids() -> bytes:
     if st != TD_OK:
         raise TDError(f"td_nccl_ids failed: {st}")
     return buf.raw
+
+
+def td_test_gemm(A_bits: np.ndarray, W_bits: np.ndarray, impl: int = 0, splits: int = 1, device: int = 0):
+    """Kernel unit test: fp32 [T, N] = A . W^T for bf16 bit patterns (uint16)."""
+    A = np.ascontiguousarray(A_bits, dtype=np.uint16)
+    W = np.ascontiguousarray(W_bits, dtype=np.uint16)
+    T, K = A.shape
+    N = W.shape[0]
+    out = np.zeros((T, N), dtype=np.float32)
+    st = lib().td_test_gemm(device, _ptr(A, C.c_uint16), _ptr(W, C.c_uint16), T, N, K, impl, splits,
+                            _ptr(out, C.c_float))
+    if st != TD_OK:
+        raise TDError(f"td_test_gemm failed: {st}")
+    return out

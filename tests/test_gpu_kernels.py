@@ -1,0 +1,31 @@
+"""Kernel-level GPU checks: the tcgen05/TMA GEMM and the mma.sync baseline vs
+an fp64 product of the same bf16 operands (plain definition of a matmul)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2506_10470_b200.tdpipe import td_test_gemm  # noqa: E402
+
+
+def _bf16(rng, shape, scale=1.0):
+    x = (rng.standard_normal(shape) * scale).astype(np.float32)
+    b = torch.from_numpy(x).to(torch.bfloat16)
+    return b.view(torch.int16).numpy().view(np.uint16), b.to(torch.float64).numpy()
+
+
+@pytest.mark.parametrize("T,N,K", [(1, 128, 64), (7, 192, 128), (32, 256, 256), (64, 384, 512), (100, 128, 1024),
+                                   (128, 512, 4096), (200, 640, 320), (256, 1024, 4096), (300, 256, 576),
+                                   (2048, 1024, 1024), (513, 4096, 128)])
+@pytest.mark.parametrize("impl,splits", [(0, 1), (0, 3), (1, 1)])
+def test_gemm_vs_fp64(T, N, K, impl, splits):
+    rng = np.random.default_rng(T * 7 + N + K)
+    Ab, Af = _bf16(rng, (T, K))
+    Wb, Wf = _bf16(rng, (N, K), 1.0 / np.sqrt(K))
+    out = td_test_gemm(Ab, Wb, impl=impl, splits=splits)
+    ref = Af @ Wf.T
+    err = np.abs(out - ref).max() / max(np.abs(ref).max(), 1e-6)
+    assert err < 2e-5, err     # fp32 accumulation of exact bf16 products
