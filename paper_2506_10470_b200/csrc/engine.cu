@@ -163,12 +163,14 @@ class CudaEngine : public Engine {
   std::vector<cudaEvent_t> ev_pool_;
   size_t ev_used_ = 0;
   std::map<std::string, KernelTiming> timing_acc_;
-  std::vector<std::string> cls_names_{"decode_attn", "prefill_attn", "gemm_qkv", "gemm_o", "gemm_gu",
-                                      "gemm_down", "lm_head", "norm", "stage", "mb"};
+  std::vector<std::string> cls_names_{"decode_attn", "prefill_attn", "gemm_qkv_pre", "gemm_o_pre", "gemm_gu_pre",
+                                      "gemm_down_pre", "lm_head_pre", "norm", "stage", "mb", "gemm_qkv_dec",
+                                      "gemm_o_dec", "gemm_gu_dec", "gemm_down_dec", "lm_head_dec"};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev_;
 };
 
 enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
+constexpr int kDecOff = 8;   // decode-phase GEMM classes = prefill class + kDecOff
 
 // --------------------------------------------------------------------- init
 td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_options& o) {
@@ -508,11 +510,12 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ep.H = H_;
     ep.Hkv = Hkv_;
     ep.hd = hd_;
-    const int iq = tbegin(cQKV);
+    const int iq = tbegin(cQKV + (M.prefill ? 0 : kDecOff));
     gemm(a_, xa_, &w, w.tqkv, w.wqkv, T, nqkv, d_, ep, !M.prefill);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.prefill) {
-      PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_};
+      PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_,
+                           dm + M.o_ctx, dm + M.o_last, n, M.max_ctx};
       const int ip = tbegin(cPreAttn);
       launch_prefill_attn(pp, st_);
       tend(ip, 0, 0);
@@ -529,21 +532,21 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eo.mode = kEpiResid;
     eo.out_f32 = x_;
     eo.ldo = d_;
-    const int io = tbegin(cO);
+    const int io = tbegin(cO + (M.prefill ? 0 : kDecOff));
     gemm(ob_, xo_, &w, w.to, w.wo, T, d_, H_ * hd_, eo, !M.prefill);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
     launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
     EpiParams eg{};
     eg.mode = kEpiSwiGLU;
     eg.out_bf16 = h_;
-    const int ig = tbegin(cGU);
+    const int ig = tbegin(cGU + (M.prefill ? 0 : kDecOff));
     gemm(a_, xa_, &w, w.tgu, w.wgu, T, 2 * F_, d_, eg, !M.prefill);
     tend(ig, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
     EpiParams ed{};
     ed.mode = kEpiResid;
     ed.out_f32 = x_;
     ed.ldo = d_;
-    const int idn = tbegin(cDown);
+    const int idn = tbegin(cDown + (M.prefill ? 0 : kDecOff));
     gemm(h_, xh_, &w, w.td, w.wd, T, d_, F_, ed, !M.prefill);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     launches_ += 6;
@@ -554,7 +557,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     el.mode = kEpiF32;
     el.out_f32 = logits_;
     el.ldo = V_;
-    const int il = tbegin(cLM);
+    const int il = tbegin(cLM + (M.prefill ? 0 : kDecOff));
     gemm(a_, xa_, nullptr, tlm_, Wlm_, n, V_, d_, el, !M.prefill);
     tend(il, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
     launches_ += 2;
@@ -657,8 +660,15 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
     double kvb = 0;
     for (int i = 0; i < n; ++i) kvb += (double)(mb.q_start[i] + mb.q_len[i]);
     kvb = kvb * 2.0 * Hkv_ * hd_ * 2 + 4.0 * n * H_ * hd_;
-    for (size_t k = t0; k < timed_.size(); ++k)
+    // prefill attention FLOPs: causal QK^T and PV over each prompt, 4*H*hd per (q, k<=q) pair
+    double pf = 0;
+    for (int i = 0; i < n; ++i) pf += 0.5 * (double)mb.q_len[i] * (mb.q_len[i] + 1);
+    pf *= 4.0 * H_ * hd_;
+    const double pb = (double)M.T * (2.0 * H_ * hd_ * 2 + 2.0 * Hkv_ * hd_ * 2);
+    for (size_t k = t0; k < timed_.size(); ++k) {
       if (timed_[k].cls == cDecAttn) timed_[k].bytes = kvb;
+      if (timed_[k].cls == cPreAttn) { timed_[k].flops = pf; timed_[k].bytes = pb; }
+    }
   }
   cudaEventRecord(ring_ev_[r], st_);
   cudaError_t e = cudaGetLastError();

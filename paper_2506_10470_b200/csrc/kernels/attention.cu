@@ -198,83 +198,211 @@ void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ prefill
-// One warp per (query token, head): lane-per-key scores over 32-key chunks,
-// online softmax, lane-owned output dims.  Keys = positions 0..pos of the
-// token's own sequence, read from the paged cache (written by the QKV epilogue
-// of this micro-batch).
+// Varlen causal flash attention on tensor cores (mma.sync m16n8k16 bf16, fp32
+// softmax), K/V read from the paged cache the QKV epilogue just wrote.  Grid:
+// (64-query tile, sequence, head); 4 warps x 16 query rows; 64-key tiles
+// double-buffered with cp.async; S = Q K^T and O += P V with P kept in
+// registers (accumulator layout == A-fragment layout).  Prefill is < 1% of the
+// prefill FLOPs at ShareGPT lengths, so mma.sync suffices.
+namespace {
+TDP_DEV void ldsm_x4(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+TDP_DEV void ldsm_x4_t(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+TDP_DEV void mma_bf16(float* c, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
 template <int HD>
-__global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnParams p) {
-  constexpr int DPL = HD >= 32 ? HD / 32 : 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x;
-  const int h = blockIdx.y * 4 + warp;
-  if (h >= p.H) return;
-  const int G = p.H / p.Hkv;
-  const int kh = h / G;
-  const int seq = p.tok_seq[t];
-  const int pos = p.tok_pos[t];
+TDP_DEV int fswz(int r, int c) {   // 16-byte chunk index inside a [64][HD] bf16 tile
+  constexpr int CH = HD / 8;
+  int pc;
+  if constexpr (CH >= 8) pc = c ^ (r & 7);
+  else if constexpr (CH == 4) pc = c ^ ((r >> 1) & 3);
+  else pc = c ^ ((r >> 2) & 1);
+  return r * CH + pc;
+}
+}  // namespace
+
+template <int HD>
+__global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p) {
+  constexpr int BQ = 64, BKV = 64, CH = HD / 8;
+  constexpr int TILE = BQ * HD * 2;
+  extern __shared__ __align__(128) uint8_t fsm[];
+  uint8_t* sQ = fsm;
+  uint8_t* sK = fsm + TILE;          // 2 stages
+  uint8_t* sV = fsm + 3 * TILE;      // 2 stages
+  const int qt = blockIdx.x, seq = blockIdx.y, h = blockIdx.z;
+  const int L = p.seq_ctx[seq];
+  const int q0 = qt * BQ;
+  if (q0 >= L) return;
+  const int row0 = p.seq_last[seq] - L + 1;     // first token row of this sequence
+  const int G = p.H / p.Hkv, kh = h / G;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
-  __shared__ float qs[4][HD];
-  const float scale = rsqrtf((float)HD) * kLog2e;
-  for (int d = lane; d < HD; d += 32)
-    qs[warp][d] = __bfloat162float(p.q[((int64_t)t * p.H + h) * HD + d]) * scale;
-  __syncwarp();
   const int64_t head_stride = (int64_t)kBlock * HD;
-  float m = -INFINITY, l = 0.f, acc[DPL];
-#pragma unroll
-  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
-  for (int base = 0; base <= pos; base += 32) {
-    const int j = base + lane;
-    float s = -INFINITY;
-    if (j <= pos) {
-      const int blk = bt[j >> 4];
-      const bf16* kp = p.kv + (((int64_t)blk * 2) * p.Hkv + kh) * head_stride + (j & 15) * HD;
-      float dot = 0.f;
-#pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        float kf[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(kp + c * 8), kf);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dot = fmaf(qs[warp][c * 8 + i], kf[i], dot);
-      }
-      s = dot;
-    }
-    const float cmax = warp_max(s);
-    const float mn = fmaxf(m, cmax);
-    const float corr = exp2f(m - mn);     // m = -inf on the first chunk -> 0
-    const float pr = (j <= pos) ? exp2f(s - mn) : 0.f;
-    l = l * corr + warp_sum(pr);
-#pragma unroll
-    for (int i = 0; i < DPL; ++i) acc[i] *= corr;
-    const int nk = min(32, pos - base + 1);
-    for (int k = 0; k < nk; ++k) {
-      const float pk = __shfl_sync(0xffffffffu, pr, k);
-      const int jj = base + k;
-      const int blk = bt[jj >> 4];
-      const bf16* vp = p.kv + (((int64_t)blk * 2 + 1) * p.Hkv + kh) * head_stride + (jj & 15) * HD;
-#pragma unroll
-      for (int i = 0; i < DPL; ++i) {
-        const int d = lane + 32 * i;
-        if (d < HD) acc[i] = fmaf(pk, __bfloat162float(vp[d]), acc[i]);
-      }
-    }
-    m = mn;
+
+  // Q tile
+  for (int i = tid; i < BQ * CH; i += 128) {
+    const int r = i / CH, c = i % CH;
+    const int q = q0 + r;
+    const bf16* src = p.q + ((int64_t)(row0 + (q < L ? q : 0)) * p.H + h) * HD + c * 8;
+    cp_async16(sQ + fswz<HD>(r, c) * 16, src, q < L);
   }
+  auto load_kv = [&](int stage, int k0) {
+    for (int i = tid; i < BKV * CH; i += 128) {
+      const int r = i / CH, c = i % CH;
+      const int j = k0 + r;
+      const bool ok = j < L;
+      const int jj = ok ? j : 0;
+      const int64_t base = (((int64_t)bt[jj >> 4] * 2) * p.Hkv + kh) * head_stride + (jj & 15) * HD + c * 8;
+      cp_async16(sK + stage * TILE + fswz<HD>(r, c) * 16, p.kv + base, ok);
+      cp_async16(sV + stage * TILE + fswz<HD>(r, c) * 16, p.kv + base + (int64_t)p.Hkv * head_stride, ok);
+    }
+  };
+  const int last_q = min(q0 + BQ, L) - 1;
+  const int n_kt = last_q / BKV + 1;
+  load_kv(0, 0);
+  cp_async_commit();
+
+  const float sl2 = rsqrtf((float)HD) * kLog2e;
+  float o[HD / 8][4];
 #pragma unroll
-  for (int i = 0; i < DPL; ++i) {
-    const int d = lane + 32 * i;
-    if (d < HD) p.o[((int64_t)t * p.H + h) * HD + d] = __float2bfloat16_rn(acc[i] / l);
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+  uint32_t qf[HD / 16][4];
+  const int g = lane >> 2, tq = lane & 3;
+  const int qr0 = q0 + warp * 16 + g;     // this thread's two query positions: qr0, qr0 + 8
+
+  for (int kt = 0; kt < n_kt; ++kt) {
+    if (kt + 1 < n_kt) load_kv((kt + 1) & 1, (kt + 1) * BKV);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kt == 0) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ldsm_x4(qf[kk], smem_u32(sQ + fswz<HD>(warp * 16 + (lane & 15), kk * 2 + (lane >> 4)) * 16));
+    }
+    const uint8_t* K = sK + (kt & 1) * TILE;
+    const uint8_t* V = sV + (kt & 1) * TILE;
+    float s[BKV / 8][4];
+#pragma unroll
+    for (int i = 0; i < BKV / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+      for (int nb = 0; nb < BKV / 16; ++nb) {
+        uint32_t b[4];
+        const int r = nb * 16 + (lane & 7) + ((lane >> 4) << 3);
+        ldsm_x4(b, smem_u32(K + fswz<HD>(r, kk * 2 + ((lane >> 3) & 1)) * 16));
+        mma_bf16(s[2 * nb], qf[kk], b);
+        mma_bf16(s[2 * nb + 1], qf[kk], b + 2);
+      }
+    }
+    // scale, causal + length mask, online softmax (rows qr0 and qr0 + 8)
+    const int k0 = kt * BKV;
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int ni = 0; ni < BKV / 8; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = k0 + ni * 8 + 2 * tq + (e & 1);
+        const int qp = qr0 + (e >> 1) * 8;
+        const float v = (key <= qp && key < L) ? s[ni][e] * sl2 : -INFINITY;
+        s[ni][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    float corr[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], 1));
+      mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], 2));
+      const float mn = fmaxf(m_r[rr], mx[rr]);
+      corr[rr] = mn == -INFINITY ? 1.f : exp2f(m_r[rr] - mn);
+      m_r[rr] = mn;
+    }
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int ni = 0; ni < BKV / 8; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float mm = m_r[e >> 1];
+        const float pv = mm == -INFINITY ? 0.f : exp2f(s[ni][e] - mm);
+        s[ni][e] = pv;
+        rs[e >> 1] += pv;
+      }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], 1);
+      rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], 2);
+      l_r[rr] = l_r[rr] * corr[rr] + rs[rr];
+    }
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      o[i][0] *= corr[0];
+      o[i][1] *= corr[0];
+      o[i][2] *= corr[1];
+      o[i][3] *= corr[1];
+    }
+    // O += P V
+#pragma unroll
+    for (int kk = 0; kk < BKV / 16; ++kk) {
+      uint32_t a[4];
+      a[0] = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
+      a[1] = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
+      a[2] = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+      a[3] = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+      for (int dn = 0; dn < HD / 16; ++dn) {
+        uint32_t b[4];
+        const int r = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        ldsm_x4_t(b, smem_u32(V + fswz<HD>(r, dn * 2 + (lane >> 4)) * 16));
+        mma_bf16(o[2 * dn], a, b);
+        mma_bf16(o[2 * dn + 1], a, b + 2);
+      }
+    }
+    __syncthreads();
   }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int q = qr0 + rr * 8;
+    if (q >= L) continue;
+    const float inv = 1.f / l_r[rr];
+    bf16* dst = p.o + ((int64_t)(row0 + q) * p.H + h) * HD;
+#pragma unroll
+    for (int ni = 0; ni < HD / 8; ++ni)
+      *reinterpret_cast<uint32_t*>(dst + ni * 8 + 2 * tq) = pack_bf16x2(o[ni][2 * rr] * inv, o[ni][2 * rr + 1] * inv);
+  }
+}
+
+template <int HD>
+static void launch_flash(const PrefillAttnParams& p, cudaStream_t st) {
+  constexpr int smem = 5 * 64 * HD * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(flash_prefill_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  dim3 grid((p.max_len + 63) / 64, p.n_seqs, p.H);
+  flash_prefill_kernel<HD><<<grid, 128, smem, st>>>(p);
 }
 
 void launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t st) {
   if (p.T <= 0) return;
-  dim3 grid(p.T, (p.H + 3) / 4);
   switch (p.hd) {
-    case 16: prefill_attn_kernel<16><<<grid, 128, 0, st>>>(p); break;
-    case 32: prefill_attn_kernel<32><<<grid, 128, 0, st>>>(p); break;
-    case 64: prefill_attn_kernel<64><<<grid, 128, 0, st>>>(p); break;
-    case 128: prefill_attn_kernel<128><<<grid, 128, 0, st>>>(p); break;
+    case 16: launch_flash<16>(p, st); break;
+    case 32: launch_flash<32>(p, st); break;
+    case 64: launch_flash<64>(p, st); break;
+    case 128: launch_flash<128>(p, st); break;
   }
 }
 

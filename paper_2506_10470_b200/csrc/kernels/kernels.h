@@ -73,6 +73,9 @@ struct PrefillAttnParams {
   int maxblk;
   bf16* o;                  // [T, H*hd]
   int T, H, Hkv, hd;
+  const int32_t* seq_ctx;   // [n] sequence length (prefill: q_start = 0)
+  const int32_t* seq_last;  // [n] row of the sequence's last token
+  int n_seqs, max_len;
 };
 void launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t st);
 

@@ -144,7 +144,7 @@ def test_td_run_batch_invariance(tmp_path):
     write_profile_csv(csv, *synthetic_profile(64, 2048, knee=8))
     outs = []
     for W, steal in [(1, 1), (2, 1), (2, 0)]:
-        _, toks, _, _ = _tiny_run(shape.with_layers(2), wl, W, csv, kv_blocks=400)
+        _, toks, _, _ = _tiny_run(shape.with_layers(2), wl, W, csv, kv_blocks=400, steal=steal)
         outs.append(toks)
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
@@ -155,7 +155,7 @@ def test_td_run_evictions_teacher_forced(tmp_path):
     """KV-starved run (C1b-like): P->D, D->P, steals and recompute evictions all
     happen; outputs still match the oracle under teacher forcing and the log is
     bit-exact."""
-    shape = SHAPES["tiny_gqa"].with_layers(2)
+    shape = SHAPES["tiny_gqa"].with_layers(3)
     csv = str(tmp_path / "p.csv")
     tables = synthetic_profile(64, 2048, knee=8)
     write_profile_csv(csv, *tables)
