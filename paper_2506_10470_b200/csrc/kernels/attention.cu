@@ -34,6 +34,8 @@ decode_attn_kernel(DecodeAttnParams p) {
   constexpr int TPW = 32 / LPT;        // tokens per warp per step
   constexpr int NW = 4;
   constexpr int U = 4;                 // tokens in flight per thread group
+  pdl_trigger();
+  pdl_wait();
   const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
   const int ctx = p.ctx[seq];
   const int n_splits = (ctx + kSplit - 1) / kSplit;
@@ -154,6 +156,8 @@ decode_attn_kernel(DecodeAttnParams p) {
 }
 
 __global__ void decode_combine_kernel(DecodeAttnParams p, int hd) {
+  pdl_trigger();
+  pdl_wait();
   const int seq = blockIdx.y, h = blockIdx.x;
   const int ctx = p.ctx[seq];
   const int n_splits = (ctx + kSplit - 1) / kSplit;
@@ -178,13 +182,13 @@ static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
   const int G = p.H / p.Hkv;
   dim3 grid(p.max_splits, p.Hkv, p.n);
   switch (G) {
-    case 1: decode_attn_kernel<HD, 1><<<grid, 128, 0, st>>>(p); break;
-    case 2: decode_attn_kernel<HD, 2><<<grid, 128, 0, st>>>(p); break;
-    case 4: decode_attn_kernel<HD, 4><<<grid, 128, 0, st>>>(p); break;
-    case 8: decode_attn_kernel<HD, 8><<<grid, 128, 0, st>>>(p); break;
+    case 1: launch_k(decode_attn_kernel<HD, 1>, grid, dim3(128), 0, st, p); break;
+    case 2: launch_k(decode_attn_kernel<HD, 2>, grid, dim3(128), 0, st, p); break;
+    case 4: launch_k(decode_attn_kernel<HD, 4>, grid, dim3(128), 0, st, p); break;
+    case 8: launch_k(decode_attn_kernel<HD, 8>, grid, dim3(128), 0, st, p); break;
     default: return;
   }
-  if (p.max_splits > 1) decode_combine_kernel<<<dim3(p.H, p.n), 128, 0, st>>>(p, HD);
+  if (p.max_splits > 1) launch_k(decode_combine_kernel, dim3(p.H, p.n), dim3(128), 0, st, p, HD);
 }
 
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {
@@ -239,6 +243,8 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
   uint8_t* sQ = fsm;
   uint8_t* sK = fsm + TILE;          // 2 stages
   uint8_t* sV = fsm + 3 * TILE;      // 2 stages
+  pdl_trigger();
+  pdl_wait();
   const int qt = blockIdx.x, seq = blockIdx.y, h = blockIdx.z;
   const int L = p.seq_ctx[seq];
   const int q0 = qt * BQ;
@@ -393,7 +399,7 @@ static void launch_flash(const PrefillAttnParams& p, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((p.max_len + 63) / 64, p.n_seqs, p.H);
-  flash_prefill_kernel<HD><<<grid, 128, smem, st>>>(p);
+  launch_k(flash_prefill_kernel<HD>, grid, dim3(128), smem, st, p);
 }
 
 void launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t st) {

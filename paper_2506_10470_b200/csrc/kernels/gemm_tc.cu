@@ -105,6 +105,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* accf = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
 
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128;
   const int n0 = blockIdx.y * BN;
@@ -135,7 +136,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
+      // weights do not depend on the previous kernel: stream the first stages
+      // before waiting for it (PDL), then the activation tiles
+      const int pre = min(nkb, STAGES);
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* sa = smem + i * STAGE_BYTES;
+        mbar_expect_tx(&full[i], STAGE_BYTES);
+        tma_load_2d(sa, &tmW, (kb0 + i) * BK, m0, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(smem + i * STAGE_BYTES + A_BYTES, &tmX, (kb0 + i) * BK, n0, &full[i]);
+      for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
@@ -146,6 +158,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
+    pdl_wait();
     if (lane == 0) {
       // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=BN
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -167,6 +180,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     }
   } else {
     // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    pdl_wait();
     mbar_wait(accf, 0);
     tc_fence_after();
     const int q = warp & 3;
@@ -203,6 +217,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 }
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t pairs = (int64_t)T * (Nf >> 1);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
     const int t = (int)(i / (Nf >> 1));
@@ -236,11 +252,11 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   const int kps = (kb_total + splits - 1) / splits;
   const int nsplit = (kb_total + kps - 1) / kps;
   dim3 grid((W.rows + 127) / 128, (T + BN - 1) / BN, nsplit);
-  kern<<<grid, 192, sm, st>>>(W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr);
+  launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr);
   if (nsplit > 1) {
     const int64_t pairs = (int64_t)T * (W.rows / 2);
     int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, nsplit, T, W.rows, ep);
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, ws, nsplit, T, W.rows, ep);
   }
 }
 }  // namespace

@@ -5,10 +5,22 @@
 // pre-norm) in fp32 from the fp32 residual.
 #include <float.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace tdp {
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TDPIPE_PDL");
+    on = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return on == 1;
+}
 
 // splitmix64 finaliser (counter-based; both sides implement it independently)
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -67,6 +79,8 @@ void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st) {
 // ----------------------------------------------------------------- embedding
 __global__ void embed_kernel(const int32_t* __restrict__ arena, const int32_t* __restrict__ tok_idx,
                              const bf16* __restrict__ E, float* __restrict__ x, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int tok = arena[tok_idx[t]];
   const uint4* src = reinterpret_cast<const uint4*>(E + (int64_t)tok * d);
@@ -82,7 +96,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ arena, const int32_t* _
 void launch_embed(const int32_t* arena, const int32_t* tok_idx, const bf16* E, float* x, int T, int d,
                   cudaStream_t st) {
   if (T <= 0) return;
-  embed_kernel<<<T, 128, 0, st>>>(arena, tok_idx, E, x, d);
+  launch_k(embed_kernel, dim3(T), dim3(128), 0, st, arena, tok_idx, E, x, d);
 }
 
 // ------------------------------------------------------------------- RMSNorm
@@ -90,6 +104,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
                                                      bf16* __restrict__ out, const int32_t* __restrict__ rows,
                                                      int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   const int r = rows ? rows[i] : i;
   const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)r * d);
@@ -125,12 +141,14 @@ __global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x
 void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* rows, int n, int d, float eps,
                     cudaStream_t st) {
   if (n <= 0) return;
-  rmsnorm_kernel<256><<<n, 256, 0, st>>>(x, g, out, rows, d, eps);
+  launch_k(rmsnorm_kernel<256>, dim3(n), dim3(256), 0, st, x, g, out, rows, d, eps);
 }
 
 // -------------------------------------------------------------------- argmax
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ arena,
                               const int32_t* __restrict__ outpos) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   const float* l = logits + (int64_t)i * V;
   float best = -FLT_MAX;
@@ -165,7 +183,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* 
 
 void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int32_t* outpos, cudaStream_t st) {
   if (n <= 0) return;
-  argmax_kernel<<<n, 256, 0, st>>>(logits, V, arena, outpos);
+  launch_k(argmax_kernel, dim3(n), dim3(256), 0, st, logits, V, arena, outpos);
 }
 
 }  // namespace tdp
