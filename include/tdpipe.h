@@ -203,9 +203,11 @@ td_status td_get_timing(struct td_ctx* ctx, const char* name, int64_t* launches,
                         double* total_ms, double* bytes, double* flops);
 
 /* Kernel unit test (testing only): out[T, N] fp32 = A[T, K] . W[N, K]^T with
- * A, W given as bf16 bit patterns (host).  impl 0 = tcgen05/TMA kernel,
+ * A, W given as bf16 bit patterns (host).  impl 0 = tcgen05 kernel,
  * 1 = mma.sync baseline; splits > 1 exercises the split-K reduction.  Runs on
- * `device`, allocates and frees its own buffers, synchronous. */
+ * `device`, allocates and frees its own buffers, synchronous.  impl 0 packs W
+ * into the tile-packed layout the engine uses; impl 2 = tcgen05 with row-major
+ * W through a TMA descriptor. */
 td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N, int32_t K,
                        int32_t impl, int32_t splits, float* out);
 

@@ -130,7 +130,6 @@ class CudaEngine : public Engine {
   XOps xa_, xo_, xh_;
   float* ws_ = nullptr;
   int64_t ws_cap_ = 0;
-  bool use_mma_ = false;
   // work
   int64_t capT_ = 0, capN_ = 0, capBlk_ = 0;
   float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
@@ -202,61 +201,61 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   }
   // ---- weights
   const int64_t nqkv = (int64_t)(H_ + 2 * Hkv_) * hd_;
-  const int64_t per_layer = nqkv * d_ + (int64_t)d_ * H_ * hd_ + 2LL * F_ * d_ + (int64_t)d_ * F_ + 2LL * d_;
-  const int64_t glob = (int64_t)V_ * d_ * 2 + d_;
+  auto pad = [](int64_t r) { return (r + 127) / 128 * 128; };   // packed weights: rows padded to 128
+  const int64_t per_layer = pad(nqkv) * d_ + pad(d_) * H_ * hd_ + pad(2LL * F_) * d_ + pad(d_) * F_ + 2LL * d_;
+  const int64_t glob = (int64_t)V_ * d_ + pad(V_) * d_ + d_;
   const int64_t nelem = per_layer * s.n_layers + glob;
   weight_bytes_ = nelem * 2;
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
   if ((double)weight_bytes_ > 0.9 * fr) { error = "weights do not fit"; return TD_ENOMEM; }
   CK(cudaMalloc(&wbuf_, nelem * 2));
+  CK(cudaMemsetAsync(wbuf_, 0, nelem * 2, st_));   // zero the packed-tile row padding
   bf16* p = wbuf_;
   auto take = [&](int64_t n) { bf16* r = p; p += n; return r; };
   const int L = s.n_layers;
   auto tid = [&](int layer, int which) { return 1 + 9 * layer + which; };
   for (int i = 0; i < L; ++i) {
     LayerW w;
-    w.wqkv = take(nqkv * d_);
-    w.wo = take((int64_t)d_ * H_ * hd_);
-    w.wgu = take(2LL * F_ * d_);
-    w.wd = take((int64_t)d_ * F_);
+    w.wqkv = take(pad(nqkv) * d_);
+    w.wo = take(pad(d_) * H_ * hd_);
+    w.wgu = take(pad(2LL * F_) * d_);
+    w.wd = take(pad(d_) * F_);
     w.g1 = take(d_);
     w.g2 = take(d_);
     L_.push_back(w);
     auto sc = [](int fan_in) { return std::sqrt(3.0f / (float)fan_in); };
-    InitSpec a{kMapQKV, kInitProj, (int)nqkv, d_, tid(i, 1), tid(i, 2), tid(i, 3), H_, Hkv_, hd_, sc(d_)};
+    InitSpec a{kMapQKV, kInitProj, (int)nqkv, d_, tid(i, 1), tid(i, 2), tid(i, 3), H_, Hkv_, hd_, sc(d_), 1};
     launch_init(w.wqkv, a, o.weight_seed, st_);
-    InitSpec b{kMapIdentity, kInitProj, d_, H_ * hd_, tid(i, 4), 0, 0, 0, 0, 0, sc(H_ * hd_)};
+    InitSpec b{kMapIdentity, kInitProj, d_, H_ * hd_, tid(i, 4), 0, 0, 0, 0, 0, sc(H_ * hd_), 1};
     launch_init(w.wo, b, o.weight_seed, st_);
-    InitSpec c{kMapGateUp, kInitProj, 2 * F_, d_, tid(i, 6), tid(i, 7), 0, 0, 0, 0, sc(d_)};
+    InitSpec c{kMapGateUp, kInitProj, 2 * F_, d_, tid(i, 6), tid(i, 7), 0, 0, 0, 0, sc(d_), 1};
     launch_init(w.wgu, c, o.weight_seed, st_);
-    InitSpec dd{kMapIdentity, kInitProj, d_, F_, tid(i, 8), 0, 0, 0, 0, 0, sc(F_)};
+    InitSpec dd{kMapIdentity, kInitProj, d_, F_, tid(i, 8), 0, 0, 0, 0, 0, sc(F_), 1};
     launch_init(w.wd, dd, o.weight_seed, st_);
-    InitSpec g1{kMapIdentity, kInitNorm, 1, d_, tid(i, 0), 0, 0, 0, 0, 0, 0.f};
+    InitSpec g1{kMapIdentity, kInitNorm, 1, d_, tid(i, 0), 0, 0, 0, 0, 0, 0.f, 0};
     launch_init(w.g1, g1, o.weight_seed, st_);
-    InitSpec g2{kMapIdentity, kInitNorm, 1, d_, tid(i, 5), 0, 0, 0, 0, 0, 0.f};
+    InitSpec g2{kMapIdentity, kInitNorm, 1, d_, tid(i, 5), 0, 0, 0, 0, 0, 0.f, 0};
     launch_init(w.g2, g2, o.weight_seed, st_);
   }
   E_ = take((int64_t)V_ * d_);
-  Wlm_ = take((int64_t)V_ * d_);
+  Wlm_ = take(pad(V_) * d_);
   gf_ = take(d_);
-  InitSpec e{kMapIdentity, kInitEmbed, V_, d_, 0, 0, 0, 0, 0, 0, 0.f};
+  InitSpec e{kMapIdentity, kInitEmbed, V_, d_, 0, 0, 0, 0, 0, 0, 0.f, 0};
   launch_init(E_, e, o.weight_seed, st_);
-  InitSpec lm{kMapIdentity, kInitProj, V_, d_, 2 + 9 * L, 0, 0, 0, 0, 0, std::sqrt(3.0f / (float)d_)};
+  InitSpec lm{kMapIdentity, kInitProj, V_, d_, 2 + 9 * L, 0, 0, 0, 0, 0, std::sqrt(3.0f / (float)d_), 1};
   launch_init(Wlm_, lm, o.weight_seed, st_);
-  InitSpec gf{kMapIdentity, kInitNorm, 1, d_, 1 + 9 * L, 0, 0, 0, 0, 0, 0.f};
+  InitSpec gf{kMapIdentity, kInitNorm, 1, d_, 1 + 9 * L, 0, 0, 0, 0, 0, 0.f, 0};
   launch_init(gf_, gf, o.weight_seed, st_);
   CK(cudaGetLastError());
-  use_mma_ = getenv("TDPIPE_GEMM") && std::string(getenv("TDPIPE_GEMM")) == "mma";
   for (int i = 0; i < L; ++i) {
     LayerW& w = L_[i];
-    if (!make_tc_operand(&w.tqkv, w.wqkv, (int)nqkv, d_, 128) || !make_tc_operand(&w.to, w.wo, d_, H_ * hd_, 128) ||
-        !make_tc_operand(&w.tgu, w.wgu, 2 * F_, d_, 128) || !make_tc_operand(&w.td, w.wd, d_, F_, 128)) {
-      error = "cuTensorMapEncodeTiled failed (weights)";
-      return TD_ECUDA;
-    }
+    w.tqkv = packed_weight(w.wqkv, (int)nqkv, d_);
+    w.to = packed_weight(w.wo, d_, H_ * hd_);
+    w.tgu = packed_weight(w.wgu, 2 * F_, d_);
+    w.td = packed_weight(w.wd, d_, F_);
   }
-  if (!make_tc_operand(&tlm_, Wlm_, V_, d_, 128)) { error = "cuTensorMapEncodeTiled failed (lm)"; return TD_ECUDA; }
+  tlm_ = packed_weight(Wlm_, V_, d_);
   // ---- RoPE table [max_seq_len][hd/2] (cos, sin), from double
   {
     const int P = s.max_seq_len, half = hd_ / 2;
@@ -352,8 +351,9 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   capT_ = T;
   capN_ = n;
   capBlk_ = maxblk;
-  // split-K workspace (decode GEMMs with few output tiles): 4 x 512 x max(Nf)
-  const int64_t wneed = 4LL * 512 * std::max<int64_t>((int64_t)(H_ + 2 * Hkv_) * hd_, d_);
+  // split-K workspace: splits * T * N <= K*N/8 (see gemm()), i.e. <= the
+  // largest weight matrix in fp32 / 4 elements
+  const int64_t wneed = std::max<int64_t>((int64_t)(H_ + 2 * Hkv_) * hd_ * d_, std::max<int64_t>(2LL * F_ * d_, (int64_t)V_ * d_)) / 8 + 1024;
   if (wneed > ws_cap_) {
     cudaFree(ws_);
     CK(cudaMalloc(&ws_, wneed * 4));
@@ -375,22 +375,24 @@ td_status CudaEngine::make_x_ops() {
   return TD_OK;
 }
 
-// Dense weight GEMM dispatch: tcgen05 kernel (default) or the mma.sync
-// baseline (TDPIPE_GEMM=mma, A/B comparisons only).  Split-K only for decode
-// micro-batches, with a count fixed by (N, K): batch-invariant.
+// Dense weight GEMM: tcgen05 kernel on tile-packed weights.
 void CudaEngine::gemm(const bf16* A, const XOps& xo, const LayerW* lw, const TcOperand& W, const bf16* Wraw, int T,
                       int N, int K, const EpiParams& ep, bool decode) {
   (void)lw;
-  if (use_mma_) {
-    launch_gemm(A, Wraw, T, N, K, ep, st_);
-    return;
-  }
+  (void)A;
+  (void)Wraw;
+  // Decode GEMMs stream weights: aim for ~2 resident CTAs per SM via split-K,
+  // capped so the fp32 partials stay <= 1/4 of the weight bytes
+  // (8*T*N*splits <= 0.25 * 2*N*K  <=>  splits <= K / (16 T)).
   int splits = 1;
-  if (decode && T <= 512) {
+  if (decode) {
     const int tiles = (N + 127) / 128;
-    splits = std::max(1, std::min(4, 148 / tiles));
-    while (splits > 1 && (K / 64) / splits < 8) --splits;
+    splits = (2 * 148 + tiles / 2) / tiles;
+    splits = std::min(splits, 16);
+    splits = std::min(splits, std::max(1, K / (16 * T)));
+    while (splits > 1 && (K / 64) / splits < 4) --splits;
     if ((int64_t)splits * T * N > ws_cap_) splits = 1;
+    splits = std::max(splits, 1);
   }
   launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, st_);
   if (splits > 1) launches_++;

@@ -56,6 +56,12 @@ TDP_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint6
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+TDP_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 TDP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 TDP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 TDP_DEV void umma_commit(uint64_t* b) {
@@ -92,9 +98,9 @@ TDP_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
 }
 
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, BN <= 128 ? 2 : 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Nf, int T,
-               int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws) {
+               int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws, const bf16* __restrict__ wpk) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
@@ -113,7 +119,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const int nkb = min(kb_per_split, kb_total - kb0);
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    if (!wpk) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -138,11 +144,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     if (lane == 0) {
       // weights do not depend on the previous kernel: stream the first stages
       // before waiting for it (PDL), then the activation tiles
+      // packed weights: this CTA's 128 rows are one contiguous run of 16 KB tiles
+      const bf16* wrow = wpk ? wpk + ((int64_t)blockIdx.x * kb_total << 13) : nullptr;
+      auto load_w = [&](uint8_t* dst, int kb, uint64_t* bar) {
+        if (wpk) bulk_load(dst, wrow + ((int64_t)kb << 13), A_BYTES, bar);
+        else tma_load_2d(dst, &tmW, kb * BK, m0, bar);
+      };
       const int pre = min(nkb, STAGES);
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = smem + i * STAGE_BYTES;
         mbar_expect_tx(&full[i], STAGE_BYTES);
-        tma_load_2d(sa, &tmW, (kb0 + i) * BK, m0, &full[i]);
+        load_w(sa, kb0 + i, &full[i]);
       }
       pdl_wait();
       for (int i = 0; i < pre; ++i)
@@ -153,7 +165,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         mbar_wait(&empty[s], ph ^ 1u);
         uint8_t* sa = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(sa, &tmW, (kb0 + i) * BK, m0, &full[s]);
+        load_w(sa, kb0 + i, &full[s]);
         tma_load_2d(sa + A_BYTES, &tmX, (kb0 + i) * BK, n0, &full[s]);
       }
     }
@@ -252,7 +264,8 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   const int kps = (kb_total + splits - 1) / splits;
   const int nsplit = (kb_total + kps - 1) / kps;
   dim3 grid((W.rows + 127) / 128, (T + BN - 1) / BN, nsplit);
-  launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr);
+  launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
+           W.packed ? W.base : nullptr);
   if (nsplit > 1) {
     const int64_t pairs = (int64_t)T * (W.rows / 2);
     int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
@@ -291,15 +304,26 @@ bool make_tc_operand(TcOperand* op, const bf16* base, int rows, int K, int box_r
   return r == CUDA_SUCCESS;
 }
 
+TcOperand packed_weight(const bf16* base, int rows, int K) {
+  TcOperand op;
+  op.base = base;
+  op.rows = rows;
+  op.K = K;
+  op.box_rows = 128;
+  op.packed = true;
+  return op;
+}
+
 int tc_bn_for(int T) { return T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
 void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
                     cudaStream_t st) {
   if (T <= 0) return;
   switch (tc_bn_for(T)) {
-    case 32: launch_bn<32, 8>(W, Xby_bn[0], T, ep, splits, ws, st); break;
-    case 64: launch_bn<64, 8>(W, Xby_bn[1], T, ep, splits, ws, st); break;
-    case 128: launch_bn<128, 6>(W, Xby_bn[2], T, ep, splits, ws, st); break;
+    // <= 110 KB of smem for BN <= 128 so that two CTAs share an SM
+    case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, st); break;
+    case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, st); break;
+    case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, st); break;
     default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, st); break;
   }
 }

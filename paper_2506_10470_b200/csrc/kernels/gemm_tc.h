@@ -13,9 +13,12 @@ struct TcOperand {
   CUtensorMap map;
   const bf16* base = nullptr;
   int rows = 0, K = 0, box_rows = 0;
+  bool packed = false;     // weights: tile-packed (kernels.h pack_offset), bulk-copied
 };
 
 bool make_tc_operand(TcOperand* op, const bf16* base, int rows, int K, int box_rows);
+// A tile-packed weight operand [rows (padded to 128), K]: no tensor map needed.
+TcOperand packed_weight(const bf16* base, int rows, int K);
 int tc_bn_for(int T);
 // out = X[T, K] . W[Nf, K]^T with epilogue ep.  Xby_bn[i] = X described with
 // box rows 32 << i.  splits > 1: split-K through workspace ws [splits][T][Nf].

@@ -18,7 +18,18 @@ struct InitSpec {
   int tid0, tid1, tid2;   // tensor ids (QKV: q,k,v; gate/up: g,u)
   int H, Hkv, hd;     // for kMapQKV
   float scale;        // sqrt_f32(3/fan_in) for projections
+  int packed;         // 1: store in the UMMA tile-packed layout (pack_offset)
 };
+
+// Tile-packed weight layout consumed by the tcgen05 GEMM: 128-row x 64-col
+// tiles (16 KB), k-tile fastest, each tile stored exactly as the 128B-swizzled
+// K-major smem image (row r, 16-byte chunk c at r*128 + ((c ^ (r & 7)) * 16)),
+// rows padded to a multiple of 128 with zeros.  A CTA therefore streams its
+// 128 rows as one contiguous run of 16 KB bulk copies.
+__host__ __device__ inline int64_t pack_offset(int64_t row, int64_t col, int64_t K) {
+  const int64_t mt = row >> 7, r = row & 127, kt = col >> 6, kk = col & 63;
+  return ((mt * (K >> 6) + kt) << 13) + r * 64 + ((((kk >> 3) ^ (r & 7))) << 3) + (kk & 7);
+}
 void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st);
 
 // ---- embedding / norms / sampling -----------------------------------------

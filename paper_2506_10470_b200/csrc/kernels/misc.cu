@@ -65,7 +65,7 @@ __global__ void init_kernel(bf16* __restrict__ dst, InitSpec s, uint64_t seed) {
     if (s.kind == kInitProj) w = __fmul_rn(s.scale, v);
     else if (s.kind == kInitNorm) w = __fadd_rn(1.0f, __fmul_rn(0.1f, v));
     else w = v;
-    dst[e] = __float2bfloat16_rn(w);
+    dst[s.packed ? pack_offset(p, c, s.cols) : e] = __float2bfloat16_rn(w);
   }
 }
 
@@ -153,9 +153,35 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* 
   const float* l = logits + (int64_t)i * V;
   float best = -FLT_MAX;
   int bi = 0x7fffffff;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) {
-    const float v = l[j];
-    if (v > best) { best = v; bi = j; }   // strided scan: first max within a thread
+  // 4 independent 16-byte loads in flight per thread; each thread visits its
+  // indices in increasing order, so '>' keeps the lowest index among ties
+  const int V4 = (V & 3) == 0 ? V >> 2 : 0;
+  const float4* l4 = reinterpret_cast<const float4*>(l);
+  int j = threadIdx.x;
+  for (; j + 3 * (int)blockDim.x < V4; j += 4 * blockDim.x) {
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = l4[j + u * blockDim.x];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = (j + u * blockDim.x) * 4;
+      if (a[u].x > best) { best = a[u].x; bi = b; }
+      if (a[u].y > best) { best = a[u].y; bi = b + 1; }
+      if (a[u].z > best) { best = a[u].z; bi = b + 2; }
+      if (a[u].w > best) { best = a[u].w; bi = b + 3; }
+    }
+  }
+  for (; j < V4; j += blockDim.x) {
+    const float4 a = l4[j];
+    const int b = j * 4;
+    if (a.x > best) { best = a.x; bi = b; }
+    if (a.y > best) { best = a.y; bi = b + 1; }
+    if (a.z > best) { best = a.z; bi = b + 2; }
+    if (a.w > best) { best = a.w; bi = b + 3; }
+  }
+  for (int k = V4 * 4 + threadIdx.x; k < V; k += blockDim.x) {
+    const float v = l[k];
+    if (v > best) { best = v; bi = k; }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -33,11 +33,26 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
     if (impl == 1) {
       launch_gemm(dA, dW, T, N, K, ep, s);
     } else {
+      // impl 0: tile-packed weights (the engine's layout); impl 2: row-major W via TMA
       TcOperand w, x[4];
-      bool ok = make_tc_operand(&w, dW, N, K, 128);
+      bool ok = true;
+      bf16* dP = nullptr;
+      if (impl == 0) {
+        const int Np = (N + 127) / 128 * 128;
+        std::vector<uint16_t> pk((size_t)Np * K, 0);
+        for (int r = 0; r < N; ++r)
+          for (int c = 0; c < K; ++c) pk[pack_offset(r, c, K)] = W[(size_t)r * K + c];
+        ok = cudaMalloc(&dP, pk.size() * 2) == cudaSuccess;
+        if (ok) cudaMemcpy(dP, pk.data(), pk.size() * 2, cudaMemcpyHostToDevice);
+        w = packed_weight(dP, N, K);
+      } else {
+        ok = make_tc_operand(&w, dW, N, K, 128);
+      }
       for (int i = 0; i < 4; ++i) ok = ok && make_tc_operand(&x[i], dA, Tcap, K, 32 << i);
       if (!ok) st = TD_ECUDA;
       else launch_gemm_tc(w, x, T, ep, splits, ws, s);
+      cudaStreamSynchronize(s);
+      cudaFree(dP);
     }
     if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
     if (st == TD_OK) cudaMemcpy(out, dO, (size_t)T * N * 4, cudaMemcpyDeviceToHost);

@@ -20,7 +20,7 @@ def _bf16(rng, shape, scale=1.0):
 @pytest.mark.parametrize("T,N,K", [(1, 128, 64), (7, 192, 128), (32, 256, 256), (64, 384, 512), (100, 128, 1024),
                                    (128, 512, 4096), (200, 640, 320), (256, 1024, 4096), (300, 256, 576),
                                    (2048, 1024, 1024), (513, 4096, 128)])
-@pytest.mark.parametrize("impl,splits", [(0, 1), (0, 3), (1, 1)])
+@pytest.mark.parametrize("impl,splits", [(0, 1), (0, 3), (2, 1), (2, 2), (1, 1)])
 def test_gemm_vs_fp64(T, N, K, impl, splits):
     rng = np.random.default_rng(T * 7 + N + K)
     Ab, Af = _bf16(rng, (T, K))
