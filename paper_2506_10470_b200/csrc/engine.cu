@@ -130,6 +130,7 @@ class CudaEngine : public Engine {
   XOps xa_, xo_, xh_;
   float* ws_ = nullptr;
   int64_t ws_cap_ = 0;
+  int* counters_ = nullptr;
   // work
   int64_t capT_ = 0, capN_ = 0, capBlk_ = 0;
   float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
@@ -307,6 +308,7 @@ void CudaEngine::release() {
   cudaFree(h_);
   cudaFree(arena_);
   cudaFree(ws_);
+  cudaFree(counters_);
   for (int i = 0; i < kRing; ++i) {
     if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
     cudaFree(dmeta_[i]);
@@ -351,13 +353,16 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   capT_ = T;
   capN_ = n;
   capBlk_ = maxblk;
-  // split-K workspace: splits * T * N <= K*N/8 (see gemm()), i.e. <= the
-  // largest weight matrix in fp32 / 4 elements
-  const int64_t wneed = std::max<int64_t>((int64_t)(H_ + 2 * Hkv_) * hd_ * d_, std::max<int64_t>(2LL * F_ * d_, (int64_t)V_ * d_)) / 8 + 1024;
+  // split-K workspace (L2-resident partial tiles) + per-tile tickets
+  const int64_t wneed = 16LL << 20;   // 64 MB of fp32; gemm() falls back to fewer splits beyond it
   if (wneed > ws_cap_) {
     cudaFree(ws_);
     CK(cudaMalloc(&ws_, wneed * 4));
     ws_cap_ = wneed;
+  }
+  if (!counters_) {
+    CK(cudaMalloc(&counters_, (1 << 16) * sizeof(int)));
+    CK(cudaMemsetAsync(counters_, 0, (1 << 16) * sizeof(int), st_));
   }
   return make_x_ops();
 }
@@ -381,21 +386,21 @@ void CudaEngine::gemm(const bf16* A, const XOps& xo, const LayerW* lw, const TcO
   (void)lw;
   (void)A;
   (void)Wraw;
-  // Decode GEMMs stream weights: aim for ~2 resident CTAs per SM via split-K,
-  // capped so the fp32 partials stay <= 1/4 of the weight bytes
-  // (8*T*N*splits <= 0.25 * 2*N*K  <=>  splits <= K / (16 T)).
+  // Decode GEMMs stream weights: aim for ~2 resident CTAs per SM via split-K
+  // (partials stay in L2; capped at the weight bytes: 8*T*N*s <= 2*N*K).
   int splits = 1;
   if (decode) {
-    const int tiles = (N + 127) / 128;
-    splits = (2 * 148 + tiles / 2) / tiles;
+    const int bn = tc_bn_for(T, true);
+    const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
+    splits = (int)((2 * 148 + ctas / 2) / ctas);
     splits = std::min(splits, 16);
-    splits = std::min(splits, std::max(1, K / (16 * T)));
+    splits = std::min(splits, std::max(1, K / (4 * T)));
     while (splits > 1 && (K / 64) / splits < 4) --splits;
-    if ((int64_t)splits * T * N > ws_cap_) splits = 1;
+    while (splits > 1 && ((int64_t)splits * ctas * 128 * bn > ws_cap_ || ctas > (1 << 16))) --splits;
     splits = std::max(splits, 1);
   }
-  launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, st_);
-  if (splits > 1) launches_++;
+  launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, counters_, decode, st_);
+
 }
 
 // -------------------------------------------------------------------- ring

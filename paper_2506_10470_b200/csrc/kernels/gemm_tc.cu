@@ -15,9 +15,9 @@
 // Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
 // w2..w5 epilogue (TMEM lane quarter = warp % 4).
 //
-// Split-K (decode only, count fixed per (Nf, K) so results do not depend on
-// the batch): partial fp32 tiles go to a workspace, reduced in split order by
-// splitk_reduce_kernel which applies the same epilogue.
+// Split-K (decode only): every split CTA writes its fp32 partial tile to an
+// L2-resident workspace; the last CTA of the tile (atomic ticket) sums the
+// partials in split order -- deterministic -- and applies the epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -56,12 +56,20 @@ TDP_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint6
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-TDP_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+TDP_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
+// weights are streamed once per step: evict-first keeps KV / activations / split-K partials in L2
+TDP_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+TDP_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 TDP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 TDP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 TDP_DEV void umma_commit(uint64_t* b) {
@@ -100,7 +108,8 @@ TDP_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, BN <= 128 ? 2 : 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Nf, int T,
-               int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws, const bf16* __restrict__ wpk) {
+               int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws, const bf16* __restrict__ wpk,
+               int* __restrict__ counters) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
@@ -110,11 +119,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* empty = full + STAGES;
   uint64_t* accf = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * 128;
-  const int n0 = blockIdx.y * BN;
+  // grid: x = token tile (fastest, so CTAs sharing a weight tile run together
+  // and the re-read hits L2), y = 128-row weight tile, z = K split
+  const int m0 = blockIdx.y * 128;
+  const int n0 = blockIdx.x * BN;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = min(kb_per_split, kb_total - kb0);
 
@@ -145,9 +157,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       // weights do not depend on the previous kernel: stream the first stages
       // before waiting for it (PDL), then the activation tiles
       // packed weights: this CTA's 128 rows are one contiguous run of 16 KB tiles
-      const bf16* wrow = wpk ? wpk + ((int64_t)blockIdx.x * kb_total << 13) : nullptr;
+      const bf16* wrow = wpk ? wpk + ((int64_t)blockIdx.y * kb_total << 13) : nullptr;
+      const uint64_t pol = policy_evict_first();
       auto load_w = [&](uint8_t* dst, int kb, uint64_t* bar) {
-        if (wpk) bulk_load(dst, wrow + ((int64_t)kb << 13), A_BYTES, bar);
+        if (wpk) bulk_load(dst, wrow + ((int64_t)kb << 13), A_BYTES, bar, pol);
         else tma_load_2d(dst, &tmW, kb * BK, m0, bar);
       };
       const int pre = min(nkb, STAGES);
@@ -198,17 +211,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int q = warp & 3;
     const int f = m0 + q * 32 + lane;            // this lane's output feature
     const bool even = (lane & 1) == 0;
+    const int nsplit = gridDim.z;
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    // split-K partial tile layout: [tile][split][128 features][BN tokens] fp32
+    float* mypart = ws ? ws + (((int64_t)tile * nsplit + blockIdx.z) * 128 + q * 32 + lane) * BN : nullptr;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
       if (ws) {
-        // split-K partial: ws[split][t][f]
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int t = n0 + c + j;
-          if (t < T && f < Nf) ws[((int64_t)blockIdx.z * T + t) * Nf + f] = __uint_as_float(r[j]);
-        }
+        for (int j = 0; j < 32; j += 4)
+          __stcg(reinterpret_cast<float4*>(mypart + c + j),
+                 make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                             __uint_as_float(r[j + 3])));
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -217,6 +233,42 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           const int t = n0 + c + j;
           if (even && t < T) epilogue_pair(ep, T, Nf, t, f, v, vp);
         }
+      }
+    }
+    if (ws) {
+      // the last CTA of this tile reduces the partials (still in L2) in split
+      // order -- deterministic whatever the arrival order -- and applies the epilogue
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (warp == 2 && lane == 0) *s_last = (atomicAdd(&counters[tile], 1) == nsplit - 1);
+      named_bar_sync(1, 128);
+      if (*s_last) {
+        __threadfence();
+        const float* base = ws + ((int64_t)tile * nsplit * 128 + q * 32 + lane) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float acc[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+          for (int z = 0; z < nsplit; ++z) {
+            const float* pz = base + (int64_t)z * 128 * BN + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(pz + j));
+              acc[j] += v.x;
+              acc[j + 1] += v.y;
+              acc[j + 2] += v.z;
+              acc[j + 3] += v.w;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float vp = __shfl_xor_sync(0xffffffffu, acc[j], 1);
+            const int t = n0 + c + j;
+            if (even && t < T) epilogue_pair(ep, T, Nf, t, f, acc[j], vp);
+          }
+        }
+        if (warp == 2 && lane == 0) counters[tile] = 0;   // ready for the next GEMM
       }
     }
     tc_fence_before();
@@ -228,31 +280,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   }
 }
 
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t pairs = (int64_t)T * (Nf >> 1);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(i / (Nf >> 1));
-    const int f = (int)(i % (Nf >> 1)) * 2;
-    float v0 = 0.f, v1 = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const float2 p = *reinterpret_cast<const float2*>(ws + ((int64_t)s * T + t) * Nf + f);
-      v0 += p.x;
-      v1 += p.y;
-    }
-    epilogue_pair(ep, T, Nf, t, f, v0, v1);
-  }
-}
-
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-  return STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
+  return STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;   // + alignment + barriers
 }
 
 template <int BN, int STAGES>
 void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, int splits, float* ws,
-               cudaStream_t st) {
+               int* counters, cudaStream_t st) {
   auto kern = gemm_tc_kernel<BN, STAGES>;
   static bool attr = false;
   constexpr int sm = smem_bytes<BN, STAGES>();
@@ -263,14 +298,9 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   const int kb_total = W.K / BK;
   const int kps = (kb_total + splits - 1) / splits;
   const int nsplit = (kb_total + kps - 1) / kps;
-  dim3 grid((W.rows + 127) / 128, (T + BN - 1) / BN, nsplit);
+  dim3 grid((T + BN - 1) / BN, (W.rows + 127) / 128, nsplit);
   launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
-           W.packed ? W.base : nullptr);
-  if (nsplit > 1) {
-    const int64_t pairs = (int64_t)T * (W.rows / 2);
-    int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
-    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, ws, nsplit, T, W.rows, ep);
-  }
+           W.packed ? W.base : nullptr, counters);
 }
 }  // namespace
 
@@ -314,17 +344,24 @@ TcOperand packed_weight(const bf16* base, int rows, int K) {
   return op;
 }
 
-int tc_bn_for(int T) { return T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
+// decode: token tiles of <= 128 (2 CTAs per SM, weight tiles shared through L2);
+// prefill: 256-token tiles
+int tc_bn_for(int T, bool decode) {
+  if (T <= 32) return 32;
+  if (T <= 64) return 64;
+  if (T <= 128 || decode) return 128;
+  return 256;
+}
 
 void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
-                    cudaStream_t st) {
+                    int* counters, bool decode, cudaStream_t st) {
   if (T <= 0) return;
-  switch (tc_bn_for(T)) {
+  switch (tc_bn_for(T, decode)) {
     // <= 110 KB of smem for BN <= 128 so that two CTAs share an SM
-    case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, st); break;
-    case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, st); break;
-    case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, st); break;
-    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, st); break;
+    case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, st); break;
+    case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, counters, st); break;
+    case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, counters, st); break;
+    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, st); break;
   }
 }
 

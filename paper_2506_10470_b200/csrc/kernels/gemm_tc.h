@@ -19,10 +19,11 @@ struct TcOperand {
 bool make_tc_operand(TcOperand* op, const bf16* base, int rows, int K, int box_rows);
 // A tile-packed weight operand [rows (padded to 128), K]: no tensor map needed.
 TcOperand packed_weight(const bf16* base, int rows, int K);
-int tc_bn_for(int T);
+int tc_bn_for(int T, bool decode);
 // out = X[T, K] . W[Nf, K]^T with epilogue ep.  Xby_bn[i] = X described with
-// box rows 32 << i.  splits > 1: split-K through workspace ws [splits][T][Nf].
+// box rows 32 << i.  splits > 1: split-K through workspace ws
+// [tiles][splits][128][BN] fp32 and zero-initialised per-tile counters.
 void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
-                    cudaStream_t st);
+                    int* counters, bool decode, cudaStream_t st);
 
 }  // namespace tdp

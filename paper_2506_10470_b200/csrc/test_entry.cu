@@ -15,15 +15,19 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
   if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
   bf16 *dA = nullptr, *dW = nullptr;
   float *dO = nullptr, *ws = nullptr;
+  int* cnt = nullptr;
   const int Tcap = ((T + 255) / 256) * 256;
   td_status st = TD_OK;
   cudaStream_t s;
   cudaStreamCreate(&s);
   if (cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dW, (size_t)N * K * 2) ||
-      cudaMalloc(&dO, (size_t)T * N * 4) || cudaMalloc(&ws, (size_t)std::max(splits, 1) * T * N * 4)) {
+      cudaMalloc(&dO, (size_t)T * N * 4) ||
+      cudaMalloc(&ws, (size_t)std::max(splits, 1) * (Tcap + 256) * ((N + 127) / 128 * 128) * 4) ||
+      cudaMalloc(&cnt, 65536 * sizeof(int))) {
     st = TD_ENOMEM;
   } else {
     cudaMemset(dA, 0, (size_t)Tcap * K * 2);
+    cudaMemset(cnt, 0, 65536 * sizeof(int));
     cudaMemcpy(dA, A, (size_t)T * K * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dW, W, (size_t)N * K * 2, cudaMemcpyHostToDevice);
     EpiParams ep{};
@@ -50,7 +54,7 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
       }
       for (int i = 0; i < 4; ++i) ok = ok && make_tc_operand(&x[i], dA, Tcap, K, 32 << i);
       if (!ok) st = TD_ECUDA;
-      else launch_gemm_tc(w, x, T, ep, splits, ws, s);
+      else launch_gemm_tc(w, x, T, ep, splits, ws, cnt, splits > 1, s);
       cudaStreamSynchronize(s);
       cudaFree(dP);
     }
@@ -61,6 +65,7 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
   cudaFree(dW);
   cudaFree(dO);
   cudaFree(ws);
+  cudaFree(cnt);
   cudaStreamDestroy(s);
   return st;
 }
