@@ -272,7 +272,75 @@ def run_ours(args):
 
 
 def run_ours_multiprocess(args, world, rank):
-    raise SystemExit("multi-process pipeline: see bench_mp (not built in this revision)")
+    """N > 1: one process per GPU = one pipeline stage (torchrun).  The
+    controller is replicated on every rank (decisions depend only on logical
+    events), the fp32 residual moves stage -> stage and the sampled tokens
+    last -> stage 0 over the library's own NCCL communicators.  torch.distributed
+    only distributes the NCCL ids and takes the max of the per-rank times."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_10470_b200 as tp
+    from paper_2506_10470_b200 import TDPipe, td_nccl_ids
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ids = [td_nccl_ids() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    peaks = load_peaks()
+    shape = SHAPES[args.model]
+    wl = config_workload(args.config)
+    n_req = len(wl.requests)
+    policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
+              "ppsb_alt": tp.TD_POLICY_PPSB_ALT}[args.policy]
+    import ctypes
+    idbuf = ctypes.create_string_buffer(ids[0], 256)
+    t = TDPipe(shape, world, device=local, policy=policy, eq2_bubble_scale=args.sigma, world_size=world, rank=rank,
+               nccl_ids=ctypes.cast(idbuf, ctypes.c_void_p))
+    L = np.array([len(r.prompt) for r in wl.requests])
+    P = np.array([r.predicted_len for r in wl.requests])
+    ctx_rep = int(L.sum() // n_req + (P.sum() // n_req) // 2)
+    t.td_profile(None, min(1024, max(n_req, 1)), 2048, ctx_rep)
+
+    def one_step():
+        t.td_reset()
+        t.submit_workload(wl)
+        t.td_upload()
+        dist.barrier()
+        torch.cuda.synchronize()
+        st = t.td_run()
+        torch.cuda.synchronize()
+        return st
+
+    for _ in range(args.warmup):
+        one_step()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    stats = [one_step() for _ in range(args.steps)]
+    clocks = sampler.stop() if sampler else None
+    dev = torch.tensor([sum(s["makespan_ns"] for s in stats) / 1e9], dtype=torch.float64, device="cuda")
+    dist.all_reduce(dev, op=dist.ReduceOp.MAX)
+    dev_s = float(dev.item())
+    gen = sum(s["generated_tokens"] for s in stats)
+    launches = torch.tensor([sum(s["gpu_launches"] for s in stats)], dtype=torch.int64, device="cuda")
+    dist.all_reduce(launches)
+    if rank == 0:
+        line = {"metric": METRIC, "value": gen / dev_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"{args.config}: {shape.name} random-init, {n_req} ShareGPT-length requests, "
+                                       f"{world}-stage TD-Pipe ({args.policy}), one process per GPU",
+                           "model": shape.name, "n_requests": n_req, "parallelism": f"pp{world}",
+                           "l2": "inputs larger than L2"},
+                "gpu_launches": int(launches.item()), "clocks": clocks,
+                "sched": {k: stats[-1][k] for k in ["n_microbatches", "n_p2d", "n_d2p", "n_stolen", "n_evicted"]},
+                "e2e": None, "roofline": None}
+        print(json.dumps(line), flush=True)
+    t.close()
+    dist.destroy_process_group()
+    return 0
 
 
 def main():

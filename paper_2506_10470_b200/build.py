@@ -21,8 +21,26 @@ LIB = os.path.join(PKG, "libtdpipe.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include():
+    """nccl.h from the torch-bundled nvidia-nccl wheel (types only; the library
+    is dlopen'ed at run time, so nothing links against libnccl)."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for loc in (spec.submodule_search_locations or []):
+            inc = os.path.join(loc, "nccl", "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return None
+
+
+NCCL_INC = _nccl_include()
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + (["-I" + NCCL_INC] if NCCL_INC else ["-DTDP_NO_NCCL"])
 CU_FLAGS = ARCH + ["-Xptxas", "-v", "--expt-relaxed-constexpr", "-diag-suppress", "177"]
 
 

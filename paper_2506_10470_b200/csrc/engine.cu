@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "nccl_rt.h"
 #include "kernels/gemm_tc.h"
 #include "kernels/kernels.h"
 
@@ -76,7 +77,7 @@ class CudaEngine : public Engine {
 
   td_status init(const td_model_shape& s, int n_stages, const td_options& o);
   int64_t kv_blocks() const override { return C_; }
-  int64_t kv_bytes_per_block() const override { return kv_block_bytes_layer_ * s_.n_layers; }
+  int64_t kv_bytes_per_block() const override { return kv_block_bytes_layer_ * (own_l1_ - own_l0_); }
   int64_t weight_bytes_stage0() const override { return weight_bytes_; }
   td_status upload(const std::vector<HostReq>& reqs) override;
   bool uploaded() const override { return uploaded_; }
@@ -115,6 +116,26 @@ class CudaEngine : public Engine {
   td_options o_{};
   int S_ = 1, hd_ = 0, H_ = 0, Hkv_ = 0, d_ = 0, F_ = 0, V_ = 0;
   std::vector<int> stage_l0_, stage_l1_;
+  // stages executed by this process: [own_s0_, own_s1_) -- all of them in
+  // single-process mode, {rank} in multi-process mode; layers [own_l0_, own_l1_)
+  int own_s0_ = 0, own_s1_ = 1, own_l0_ = 0, own_l1_ = 0;
+  int world_ = 1, rank_ = 0;
+#ifndef TDP_NO_NCCL
+  const NcclApi* nc_ = nullptr;
+  ncclComm_t cf_ = nullptr, cb_ = nullptr;   // forward (residual) / backward (tokens) comms
+#endif
+  cudaStream_t tst_ = nullptr;               // stage 0: token-return stream
+  static constexpr int kTokRing = 16;
+  int32_t* tokbuf_ = nullptr;                // [kTokRing][2 * capN]
+  cudaEvent_t tok_ev_[kTokRing] = {};
+  int64_t tok_k_ = 0;
+  bool tok_have_ = false;
+  int32_t* pairs_ = nullptr;                 // last stage: [2 * capN]
+  td_status nccl_check(int r, const char* what);
+  td_status mp_send_recv_x(bool send, int peer, int T);
+ public:
+  int returned(const MicroBatch& mb) override;
+ private:
   int dev_ = 0;
   cudaStream_t st_ = nullptr;
   // weights
@@ -183,7 +204,8 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   hd_ = d_ / H_;
   F_ = s.d_ffn;
   V_ = s.vocab;
-  if (o.world_size > 1) { error = "multi-process pipeline requires the NCCL engine"; return TD_EINVAL; }
+  world_ = o.world_size;
+  rank_ = o.rank;
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (o.device < 0 || o.device >= ndev) { error = "bad device"; return TD_ECUDA; }
@@ -200,12 +222,35 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
     l += q + (i < r ? 1 : 0);
     stage_l1_.push_back(l);
   }
-  // ---- weights
+  own_s0_ = world_ > 1 ? rank_ : 0;
+  own_s1_ = world_ > 1 ? rank_ + 1 : S_;
+  own_l0_ = stage_l0_[own_s0_];
+  own_l1_ = stage_l1_[own_s1_ - 1];
+  const bool has_embed = own_s0_ == 0, has_head = own_s1_ == S_;
+  if (world_ > 1) {
+#ifdef TDP_NO_NCCL
+    error = "built without nccl.h";
+    return TD_ENCCL;
+#else
+    if (!o.nccl_ids) { error = "world_size > 1 needs nccl_ids"; return TD_EINVAL; }
+    std::string e;
+    nc_ = nccl_api(&e);
+    if (!nc_) { error = e; return TD_ENCCL; }
+    ncclUniqueId idf, idb;
+    std::memcpy(&idf, o.nccl_ids, sizeof idf);
+    std::memcpy(&idb, static_cast<const char*>(o.nccl_ids) + 128, sizeof idb);
+    if (td_status r1 = nccl_check(nc_->commInitRank(&cf_, world_, idf, rank_), "ncclCommInitRank(fwd)")) return r1;
+    if (td_status r2 = nccl_check(nc_->commInitRank(&cb_, world_, idb, rank_), "ncclCommInitRank(bwd)")) return r2;
+    CK(cudaStreamCreateWithFlags(&tst_, cudaStreamNonBlocking));
+    for (int i = 0; i < kTokRing; ++i) CK(cudaEventCreateWithFlags(&tok_ev_[i], cudaEventDisableTiming));
+#endif
+  }
+  // ---- weights (this process's layers only; embedding on stage 0, head on the last)
   const int64_t nqkv = (int64_t)(H_ + 2 * Hkv_) * hd_;
   auto pad = [](int64_t r) { return (r + 127) / 128 * 128; };   // packed weights: rows padded to 128
   const int64_t per_layer = pad(nqkv) * d_ + pad(d_) * H_ * hd_ + pad(2LL * F_) * d_ + pad(d_) * F_ + 2LL * d_;
-  const int64_t glob = (int64_t)V_ * d_ + pad(V_) * d_ + d_;
-  const int64_t nelem = per_layer * s.n_layers + glob;
+  const int64_t glob = (has_embed ? (int64_t)V_ * d_ : 0) + (has_head ? pad(V_) * d_ + d_ : 0);
+  const int64_t nelem = per_layer * (own_l1_ - own_l0_) + glob;
   weight_bytes_ = nelem * 2;
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
@@ -216,7 +261,8 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   auto take = [&](int64_t n) { bf16* r = p; p += n; return r; };
   const int L = s.n_layers;
   auto tid = [&](int layer, int which) { return 1 + 9 * layer + which; };
-  for (int i = 0; i < L; ++i) {
+  L_.assign(L, LayerW{});
+  for (int i = own_l0_; i < own_l1_; ++i) {
     LayerW w;
     w.wqkv = take(pad(nqkv) * d_);
     w.wo = take(pad(d_) * H_ * hd_);
@@ -224,7 +270,6 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
     w.wd = take(pad(d_) * F_);
     w.g1 = take(d_);
     w.g2 = take(d_);
-    L_.push_back(w);
     auto sc = [](int fan_in) { return std::sqrt(3.0f / (float)fan_in); };
     InitSpec a{kMapQKV, kInitProj, (int)nqkv, d_, tid(i, 1), tid(i, 2), tid(i, 3), H_, Hkv_, hd_, sc(d_), 1};
     launch_init(w.wqkv, a, o.weight_seed, st_);
@@ -238,25 +283,30 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
     launch_init(w.g1, g1, o.weight_seed, st_);
     InitSpec g2{kMapIdentity, kInitNorm, 1, d_, tid(i, 5), 0, 0, 0, 0, 0, 0.f, 0};
     launch_init(w.g2, g2, o.weight_seed, st_);
+    L_[i] = w;
   }
-  E_ = take((int64_t)V_ * d_);
-  Wlm_ = take(pad(V_) * d_);
-  gf_ = take(d_);
-  InitSpec e{kMapIdentity, kInitEmbed, V_, d_, 0, 0, 0, 0, 0, 0, 0.f, 0};
-  launch_init(E_, e, o.weight_seed, st_);
-  InitSpec lm{kMapIdentity, kInitProj, V_, d_, 2 + 9 * L, 0, 0, 0, 0, 0, std::sqrt(3.0f / (float)d_), 1};
-  launch_init(Wlm_, lm, o.weight_seed, st_);
-  InitSpec gf{kMapIdentity, kInitNorm, 1, d_, 1 + 9 * L, 0, 0, 0, 0, 0, 0.f, 0};
-  launch_init(gf_, gf, o.weight_seed, st_);
+  if (has_embed) {
+    E_ = take((int64_t)V_ * d_);
+    InitSpec e{kMapIdentity, kInitEmbed, V_, d_, 0, 0, 0, 0, 0, 0, 0.f, 0};
+    launch_init(E_, e, o.weight_seed, st_);
+  }
+  if (has_head) {
+    Wlm_ = take(pad(V_) * d_);
+    gf_ = take(d_);
+    InitSpec lm{kMapIdentity, kInitProj, V_, d_, 2 + 9 * L, 0, 0, 0, 0, 0, std::sqrt(3.0f / (float)d_), 1};
+    launch_init(Wlm_, lm, o.weight_seed, st_);
+    InitSpec gf{kMapIdentity, kInitNorm, 1, d_, 1 + 9 * L, 0, 0, 0, 0, 0, 0.f, 0};
+    launch_init(gf_, gf, o.weight_seed, st_);
+  }
   CK(cudaGetLastError());
-  for (int i = 0; i < L; ++i) {
+  for (int i = own_l0_; i < own_l1_; ++i) {
     LayerW& w = L_[i];
     w.tqkv = packed_weight(w.wqkv, (int)nqkv, d_);
     w.to = packed_weight(w.wo, d_, H_ * hd_);
     w.tgu = packed_weight(w.wgu, 2 * F_, d_);
     w.td = packed_weight(w.wd, d_, F_);
   }
-  tlm_ = packed_weight(Wlm_, V_, d_);
+  if (has_head) tlm_ = packed_weight(Wlm_, V_, d_);
   // ---- RoPE table [max_seq_len][hd/2] (cos, sin), from double
   {
     const int P = s.max_seq_len, half = hd_ / 2;
@@ -276,7 +326,7 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   const int64_t T0 = std::max<int64_t>(o.prefill_token_budget, s.max_seq_len);
   if (td_status e2 = ensure_work(T0, std::min<int64_t>(o.max_batch_seqs, 1024), cdiv(s.max_seq_len, 16))) return e2;
   kv_block_bytes_layer_ = 2LL * Hkv_ * 16 * hd_ * 2;
-  const int64_t per_block = kv_block_bytes_layer_ * L;
+  const int64_t per_block = kv_block_bytes_layer_ * (own_l1_ - own_l0_);
   if (o.kv_blocks > 0) {
     C_ = o.kv_blocks;
   } else {
@@ -284,6 +334,17 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
     const double avail = (double)fr - o.hbm_reserve_frac * (double)tot - 512.0 * (1 << 20);
     C_ = (int64_t)(avail / (double)per_block);
   }
+#ifndef TDP_NO_NCCL
+  if (world_ > 1) {   // one logical block table for all stages: C = min over ranks
+    int64_t* dC = nullptr;
+    CK(cudaMalloc(&dC, sizeof(int64_t)));
+    CK(cudaMemcpyAsync(dC, &C_, sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+    if (td_status r3 = nccl_check(nc_->allReduce(dC, dC, 1, ncclInt64, ncclMin, cf_, st_), "allReduce(C)")) return r3;
+    CK(cudaMemcpyAsync(&C_, dC, sizeof(int64_t), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    cudaFree(dC);
+  }
+#endif
   if (C_ < 1) { error = "no room for the KV pool"; return TD_ENOMEM; }
   if (cudaMalloc(&kv_, C_ * per_block) != cudaSuccess) { error = "KV pool allocation failed"; return TD_ENOMEM; }
   CK(cudaMemsetAsync(kv_, 0, C_ * per_block, st_));
@@ -319,6 +380,15 @@ void CudaEngine::release() {
   for (auto& pr : stage_ev_) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (ev_end_) cudaEventDestroy(ev_end_);
+  cudaFree(tokbuf_);
+  cudaFree(pairs_);
+  for (int i = 0; i < kTokRing; ++i)
+    if (tok_ev_[i]) cudaEventDestroy(tok_ev_[i]);
+  if (tst_) { cudaStreamSynchronize(tst_); cudaStreamDestroy(tst_); }
+#ifndef TDP_NO_NCCL
+  if (nc_ && cf_) nc_->commDestroy(cf_);
+  if (nc_ && cb_) nc_->commDestroy(cb_);
+#endif
   if (st_) cudaStreamDestroy(st_);
   st_ = nullptr;
 }
@@ -350,6 +420,11 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
     }
     meta_cap_ = need;
   }
+  if (tst_) CK(cudaStreamSynchronize(tst_));
+  cudaFree(tokbuf_);
+  cudaFree(pairs_);
+  CK(cudaMalloc(&tokbuf_, (size_t)kTokRing * 2 * n * 4));
+  CK(cudaMalloc(&pairs_, (size_t)2 * n * 4));
   capT_ = T;
   capN_ = n;
   capBlk_ = maxblk;
@@ -505,7 +580,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
   }
   for (int l = stage_l0_[stage]; l < stage_l1_[stage]; ++l) {
     const LayerW& w = L_[l];
-    bf16* kvl = kv_ + (int64_t)l * C_ * (kv_block_bytes_layer_ / 2);
+    bf16* kvl = kv_ + (int64_t)(l - own_l0_) * C_ * (kv_block_bytes_layer_ / 2);
     launch_rmsnorm(x_, w.g1, a_, nullptr, T, d_, eps, st_);
     EpiParams ep{};
     ep.mode = kEpiQKV;
@@ -577,12 +652,71 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
 }
 
 td_status CudaEngine::run_microbatch(const Meta& M, const int32_t* dm, int32_t* arena) {
-  for (int s = 0; s < S_; ++s) {
+  for (int s = own_s0_; s < own_s1_; ++s) {
+    if (world_ > 1 && s > 0)   // receive the fp32 residual hand-off from stage s-1
+      if (td_status e = mp_send_recv_x(false, s - 1, M.T)) return e;
     const int is = tbegin(cStage);
     if (td_status e = run_stage(s, M, dm, arena)) return e;
     tend(is, 0, 0);
+    if (world_ > 1 && s < S_ - 1)
+      if (td_status e = mp_send_recv_x(true, s + 1, M.T)) return e;
+#ifndef TDP_NO_NCCL
+    if (world_ > 1 && s == S_ - 1) {   // sampled tokens -> stage 0 (token-return comm)
+      launch_token_pairs(arena, dm + M.o_outpos, M.n, pairs_, st_);
+      if (td_status e = nccl_check(nc_->send(pairs_, (size_t)2 * M.n, ncclInt32, 0, cb_, st_), "ncclSend(tokens)"))
+        return e;
+    }
+#endif
   }
   return TD_OK;
+}
+
+td_status CudaEngine::nccl_check(int r, const char* what) {
+#ifndef TDP_NO_NCCL
+  if (r != ncclSuccess) {
+    error = std::string(what) + ": " + (nc_ ? nc_->getErrorString((ncclResult_t)r) : "nccl");
+    return TD_ENCCL;
+  }
+#else
+  (void)r;
+  (void)what;
+#endif
+  return TD_OK;
+}
+
+td_status CudaEngine::mp_send_recv_x(bool send, int peer, int T) {
+#ifndef TDP_NO_NCCL
+  const size_t cnt = (size_t)T * d_;
+  return send ? nccl_check(nc_->send(x_, cnt, ncclFloat32, peer, cf_, st_), "ncclSend(x)")
+              : nccl_check(nc_->recv(x_, cnt, ncclFloat32, peer, cf_, st_), "ncclRecv(x)");
+#else
+  (void)send;
+  (void)peer;
+  (void)T;
+  return TD_ENCCL;
+#endif
+}
+
+// Stage 0 of a multi-process pipeline learns the tokens of micro-batch k from
+// the last stage when the controller processes k's return (in launch order on
+// every rank): receive (position, token) pairs on the token stream, scatter
+// into the arena, and let the compute stream wait on it before its next launch.
+int CudaEngine::returned(const MicroBatch& mb) {
+#ifndef TDP_NO_NCCL
+  if (world_ > 1 && own_s0_ == 0) {
+    const int n = (int)mb.members.size();
+    const int slot = (int)(tok_k_ % kTokRing);
+    int32_t* buf = tokbuf_ + (int64_t)slot * 2 * capN_;
+    if (nccl_check(nc_->recv(buf, (size_t)2 * n, ncclInt32, S_ - 1, cb_, tst_), "ncclRecv(tokens)")) return TD_ENCCL;
+    launch_token_scatter(buf, n, arena_, tst_);
+    cudaEventRecord(tok_ev_[slot], tst_);
+    tok_have_ = true;
+    ++tok_k_;
+  }
+#else
+  (void)mb;
+#endif
+  return 0;
 }
 
 // ------------------------------------------------------------------- runs
@@ -626,6 +760,8 @@ td_status CudaEngine::begin_run(const std::vector<HostReq>& reqs, bool record_lo
   ev_used_ = 0;
   started_ = false;
   for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
+  tok_k_ = 0;
+  tok_have_ = false;
   return TD_OK;
 }
 
@@ -658,6 +794,8 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
     error = "metadata H2D failed";
     return TD_ECUDA;
   }
+  if (world_ > 1 && own_s0_ == 0 && tok_have_)   // tokens of every returned micro-batch are in the arena
+    cudaStreamWaitEvent(st_, tok_ev_[(tok_k_ - 1) % kTokRing], 0);
   h2d_bytes_ += (int64_t)M.total * 4;
   const size_t t0 = timed_.size();
   if (td_status e = run_microbatch(M, dmeta_[r], arena_)) return e;
@@ -697,6 +835,13 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
 }
 
 td_status CudaEngine::end_run(td_run_stats* st) {
+  if (tst_) {   // stage 0: the last token scatter belongs to the job
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, tst_));
+    CK(cudaStreamWaitEvent(st_, e, 0));
+    cudaEventDestroy(e);
+  }
   CK(cudaEventRecord(ev_end_, st_));
   CK(cudaStreamSynchronize(st_));
   float ms = 0.f;
@@ -745,7 +890,7 @@ td_status CudaEngine::get_logits(int64_t rid, std::vector<float>* out, int* n_st
 }
 
 td_status CudaEngine::kv_reset() {
-  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * s_.n_layers, st_));
+  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * (own_l1_ - own_l0_), st_));
   CK(cudaStreamSynchronize(st_));
   return TD_OK;
 }
@@ -753,6 +898,7 @@ td_status CudaEngine::kv_reset() {
 // ----------------------------------------------------------- stage forward
 td_status CudaEngine::stage_forward(int stage, const td_batch& b, const void* in, void* out) {
   CK(cudaSetDevice(dev_));
+  if (stage < own_s0_ || stage >= own_s1_) { error = "stage not owned by this process"; return TD_EINVAL; }
   const int n = b.n_seqs;
   if (n < 1) { error = "empty batch"; return TD_EINVAL; }
   int T = 0, maxctx = 1;
@@ -818,7 +964,7 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
     Meta M = build_meta(0, prefill, n, qs.data(), ql.data(), nullptr, {}, bt.data(), nb + 1);
     CK(cudaMemcpyAsync(dmeta_[0], hmeta_[0], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_));
     int64_t worst = 0;
-    for (int s = 0; s < S_; ++s) {
+    for (int s = own_s0_; s < own_s1_; ++s) {
       std::vector<float> ts;
       for (int rep = 0; rep < 6; ++rep) {
         CK(cudaEventRecord(e0, st_));
@@ -859,6 +1005,22 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
     kval.push_back(ns);
   }
   timing_ = saved;
+#ifndef TDP_NO_NCCL
+  if (world_ > 1) {   // every rank must hold the same frozen table: per-stage max over ranks
+    std::vector<int64_t> all(bval);
+    all.insert(all.end(), kval.begin(), kval.end());
+    int64_t* dv = nullptr;
+    CK(cudaMalloc(&dv, all.size() * sizeof(int64_t)));
+    CK(cudaMemcpyAsync(dv, all.data(), all.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+    if (td_status r = nccl_check(nc_->allReduce(dv, dv, all.size(), ncclInt64, ncclMax, cf_, st_), "allReduce(profile)"))
+      return r;
+    CK(cudaMemcpyAsync(all.data(), dv, all.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    cudaFree(dv);
+    std::copy(all.begin(), all.begin() + bval.size(), bval.begin());
+    std::copy(all.begin() + bval.size(), all.end(), kval.begin());
+  }
+#endif
   auto interp = [](const std::vector<int>& g, const std::vector<int64_t>& v, int maxv, std::vector<int64_t>* out) {
     out->assign(maxv + 1, 0);
     for (int x = 1; x <= maxv; ++x) {
@@ -875,7 +1037,7 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(tok);
-  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * s_.n_layers, st_));
+  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * (own_l1_ - own_l0_), st_));
   CK(cudaStreamSynchronize(st_));
   return TD_OK;
 }

@@ -40,6 +40,9 @@ void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* row
                     cudaStream_t st);
 // tokens: arena[outpos[i]] = argmax_j logits[i][j] (lowest index on ties)
 void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int32_t* outpos, cudaStream_t st);
+// multi-process token return: pairs[2i] = outpos[i], pairs[2i+1] = arena[outpos[i]]; and its inverse
+void launch_token_pairs(const int32_t* arena, const int32_t* outpos, int n, int32_t* pairs, cudaStream_t st);
+void launch_token_scatter(const int32_t* pairs, int n, int32_t* arena, cudaStream_t st);
 
 // ---- GEMM: C[M,N] = A[M,K] . W[N,K]^T, bf16 in, fp32 accumulate ----------
 enum GemmEpi { kEpiF32 = 0, kEpiResid = 1, kEpiSwiGLU = 2, kEpiQKV = 3, kEpiBF16 = 4 };

@@ -212,4 +212,31 @@ void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int3
   launch_k(argmax_kernel, dim3(n), dim3(256), 0, st, logits, V, arena, outpos);
 }
 
+// ----------------------------------------------- token return (multi-process)
+// last stage: (arena position, token) pairs of one micro-batch -> NCCL to stage 0
+__global__ void token_pairs_kernel(const int32_t* __restrict__ arena, const int32_t* __restrict__ outpos, int n,
+                                   int32_t* __restrict__ pairs) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int p = outpos[i];
+    pairs[2 * i] = p;
+    pairs[2 * i + 1] = arena[p];
+  }
+}
+// stage 0: scatter received pairs into its token arena
+__global__ void token_scatter_kernel(const int32_t* __restrict__ pairs, int n, int32_t* __restrict__ arena) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    arena[pairs[2 * i]] = pairs[2 * i + 1];
+}
+
+void launch_token_pairs(const int32_t* arena, const int32_t* outpos, int n, int32_t* pairs, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_k(token_pairs_kernel, dim3((n + 255) / 256), dim3(256), 0, st, arena, outpos, n, pairs);
+}
+void launch_token_scatter(const int32_t* pairs, int n, int32_t* arena, cudaStream_t st) {
+  if (n <= 0) return;
+  token_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(pairs, n, arena);
+}
+
 }  // namespace tdp
