@@ -211,6 +211,13 @@ td_status td_get_timing(struct td_ctx* ctx, const char* name, int64_t* launches,
 td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N, int32_t K,
                        int32_t impl, int32_t splits, float* out);
 
+/* GEMM timing sweep (testing only): average device microseconds per call of
+ * the tcgen05 GEMM on [T, K] x [N, K]^T (tile-packed weights, fp32 output),
+ * cycling over `copies` weight buffers so that the weights stream from HBM;
+ * splits = split-K count (1 = none); decode = 1 selects decode token tiles. */
+td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t splits, int32_t decode,
+                        int32_t iters, int32_t copies, float* us_per_call);
+
 /* Generate the two ncclUniqueIds (256 bytes) rank 0 shares with all ranks. */
 td_status td_nccl_ids(void* out256);
 

@@ -15,9 +15,9 @@
 // Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
 // w2..w5 epilogue (TMEM lane quarter = warp % 4).
 //
-// Split-K (decode only): every split CTA writes its fp32 partial tile to an
-// L2-resident workspace; the last CTA of the tile (atomic ticket) sums the
-// partials in split order -- deterministic -- and applies the epilogue.
+// Split-K (decode only): partial fp32 tiles go to a workspace, reduced in
+// split order (deterministic) by splitk_reduce_kernel, which applies the
+// same fused epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -119,7 +119,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* empty = full + STAGES;
   uint64_t* accf = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -211,20 +211,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int q = warp & 3;
     const int f = m0 + q * 32 + lane;            // this lane's output feature
     const bool even = (lane & 1) == 0;
-    const int nsplit = gridDim.z;
-    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-    // split-K partial tile layout: [tile][split][128 features][BN tokens] fp32
-    float* mypart = ws ? ws + (((int64_t)tile * nsplit + blockIdx.z) * 128 + q * 32 + lane) * BN : nullptr;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
       if (ws) {
+        // split-K partial: ws[split][t][f] (lanes = consecutive features: coalesced)
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          __stcg(reinterpret_cast<float4*>(mypart + c + j),
-                 make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                             __uint_as_float(r[j + 3])));
+        for (int j = 0; j < 32; ++j) {
+          const int t = n0 + c + j;
+          if (t < T && f < Nf) __stcg(ws + ((int64_t)blockIdx.z * T + t) * Nf + f, __uint_as_float(r[j]));
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -235,48 +232,31 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
       }
     }
-    if (ws) {
-      // the last CTA of this tile reduces the partials (still in L2) in split
-      // order -- deterministic whatever the arrival order -- and applies the epilogue
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (warp == 2 && lane == 0) *s_last = (atomicAdd(&counters[tile], 1) == nsplit - 1);
-      named_bar_sync(1, 128);
-      if (*s_last) {
-        __threadfence();
-        const float* base = ws + ((int64_t)tile * nsplit * 128 + q * 32 + lane) * BN;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          float acc[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-          for (int z = 0; z < nsplit; ++z) {
-            const float* pz = base + (int64_t)z * 128 * BN + c;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(pz + j));
-              acc[j] += v.x;
-              acc[j + 1] += v.y;
-              acc[j + 2] += v.z;
-              acc[j + 3] += v.w;
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float vp = __shfl_xor_sync(0xffffffffu, acc[j], 1);
-            const int t = n0 + c + j;
-            if (even && t < T) epilogue_pair(ep, T, Nf, t, f, acc[j], vp);
-          }
-        }
-        if (warp == 2 && lane == 0) counters[tile] = 0;   // ready for the next GEMM
-      }
-    }
     tc_fence_before();
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+// split-K reduction: sums the partials in split order (deterministic) and
+// applies the fused epilogue; grid-stride over (token, feature pair)
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t pairs = (int64_t)T * (Nf >> 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / (Nf >> 1));
+    const int f = (int)(i % (Nf >> 1)) * 2;
+    float v0 = 0.f, v1 = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float2 p = __ldcg(reinterpret_cast<const float2*>(ws + ((int64_t)s * T + t) * Nf + f));
+      v0 += p.x;
+      v1 += p.y;
+    }
+    epilogue_pair(ep, T, Nf, t, f, v0, v1);
   }
 }
 
@@ -301,6 +281,11 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   dim3 grid((T + BN - 1) / BN, (W.rows + 127) / 128, nsplit);
   launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
            W.packed ? W.base : nullptr, counters);
+  if (nsplit > 1) {
+    const int64_t pairs = (int64_t)T * (W.rows / 2);
+    const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, ws, nsplit, T, W.rows, ep);
+  }
 }
 }  // namespace
 

@@ -69,3 +69,61 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
   cudaStreamDestroy(s);
   return st;
 }
+
+extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t splits, int32_t decode,
+                                   int32_t iters, int32_t copies, float* us_per_call) {
+  if (T < 1 || N < 2 || (N & 1) || K < 64 || K % 64 || iters < 1 || copies < 1 || !us_per_call) return TD_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
+  const int Np = (N + 127) / 128 * 128;
+  const int Tcap = ((T + 255) / 256) * 256;
+  std::vector<bf16*> Ws(copies, nullptr);
+  bf16* dA = nullptr;
+  float *dO = nullptr, *ws = nullptr;
+  int* cnt = nullptr;
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  td_status st = TD_OK;
+  for (auto& w : Ws)
+    if (cudaMalloc(&w, (size_t)Np * K * 2) != cudaSuccess) st = TD_ENOMEM;
+  if (st || cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dO, (size_t)T * N * 4) ||
+      cudaMalloc(&ws, (size_t)std::max(splits, 1) * (Tcap + 256) * Np * 4) || cudaMalloc(&cnt, 65536 * 4)) {
+    st = TD_ENOMEM;
+  } else {
+    for (auto& w : Ws) cudaMemset(w, 0, (size_t)Np * K * 2);
+    cudaMemset(dA, 0, (size_t)Tcap * K * 2);
+    cudaMemset(cnt, 0, 65536 * 4);
+    EpiParams ep{};
+    ep.mode = kEpiF32;
+    ep.out_f32 = dO;
+    ep.ldo = N;
+    TcOperand x[4];
+    bool ok = true;
+    for (int i = 0; i < 4; ++i) ok = ok && make_tc_operand(&x[i], dA, Tcap, K, 32 << i);
+    std::vector<TcOperand> w(copies);
+    for (int i = 0; i < copies; ++i) w[i] = packed_weight(Ws[i], N, K);
+    if (!ok) {
+      st = TD_ECUDA;
+    } else {
+      for (int i = 0; i < 3; ++i) launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode != 0, s);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+      for (int i = 0; i < iters; ++i) launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode != 0, s);
+      cudaEventRecord(b, s);
+      if (cudaEventSynchronize(b) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      *us_per_call = ms * 1000.f / iters;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  }
+  for (auto& wp : Ws) cudaFree(wp);
+  cudaFree(dA);
+  cudaFree(dO);
+  cudaFree(ws);
+  cudaFree(cnt);
+  cudaStreamDestroy(s);
+  return st;
+}

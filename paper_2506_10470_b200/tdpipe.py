@@ -62,7 +62,7 @@ class td_batch(C.Structure):
 EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td_submit", "td_upload",
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
-           "td_get_timing", "td_nccl_ids", "td_test_gemm"]
+           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_get_timing.argtypes = [C.c_void_p, C.c_char_p, P(C.c_int64), P(C.c_double), P(C.c_double),
                                   P(C.c_double)]
     lib.td_nccl_ids.argtypes = [C.c_void_p]
+    lib.td_bench_gemm.argtypes = [C.c_int32] * 8 + [P(C.c_float)]
     lib.td_test_gemm.argtypes = [C.c_int32, P(C.c_uint16), P(C.c_uint16), C.c_int32, C.c_int32, C.c_int32,
                                  C.c_int32, C.c_int32, P(C.c_float)]
     for f in EXPORTS:
@@ -286,3 +287,13 @@ def td_test_gemm(A_bits: np.ndarray, W_bits: np.ndarray, impl: int = 0, splits: 
     if st != TD_OK:
         raise TDError(f"td_test_gemm failed: {st}")
     return out
+
+
+def td_bench_gemm(T: int, N: int, K: int, splits: int = 1, decode: bool = True, iters: int = 50, copies: int = 4,
+                  device: int = 0) -> float:
+    """Average device microseconds per tcgen05 GEMM call (weights streamed from HBM)."""
+    us = C.c_float(0)
+    st = lib().td_bench_gemm(device, T, N, K, splits, int(decode), iters, copies, C.byref(us))
+    if st != TD_OK:
+        raise TDError(f"td_bench_gemm failed: {st}")
+    return us.value
