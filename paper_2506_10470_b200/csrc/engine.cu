@@ -106,8 +106,8 @@ class CudaEngine : public Engine {
   td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena);
   td_status run_microbatch(const Meta& M, const int32_t* dmeta, int32_t* arena);
   td_status make_x_ops();
-  void gemm(const bf16* A, const XOps& xo, const LayerW* lw, const TcOperand& W, const bf16* Wraw, int T, int N,
-            int K, const EpiParams& ep, bool decode);
+  int gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
+           bool defer = false);
   int tbegin(int cls);
   void tend(int idx, double bytes, double flops);
   int ring_acquire();
@@ -407,7 +407,7 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&ob_, T * H_ * hd_ * 2));
   CK(cudaMalloc(&h_, T * F_ * 2));
   CK(cudaMalloc(&logits_, n * V_ * 4));
-  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 512);
+  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 128);
   CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
   // metadata ring: per seq 5 ints + bt, per token 4 ints, header
   const int64_t need = 16 + 5 * n + 2 + n * maxblk + 4 * T + 64;
@@ -455,27 +455,24 @@ td_status CudaEngine::make_x_ops() {
   return TD_OK;
 }
 
-// Dense weight GEMM: tcgen05 kernel on tile-packed weights.
-void CudaEngine::gemm(const bf16* A, const XOps& xo, const LayerW* lw, const TcOperand& W, const bf16* Wraw, int T,
-                      int N, int K, const EpiParams& ep, bool decode) {
-  (void)lw;
-  (void)A;
-  (void)Wraw;
-  // Decode GEMMs stream weights: aim for ~2 resident CTAs per SM via split-K
-  // (partials stay in L2; capped at the weight bytes: 8*T*N*s <= 2*N*K).
+// Dense weight GEMM: tcgen05 kernel on tile-packed weights.  Decode GEMMs
+// stream weights; split-K targets ~288 CTAs (about 2 per SM), at most 8 splits
+// and >= 4 k-blocks per split (measured sweep: scripts/gemm_sweep.py).
+// Returns the split count used; with defer = true and splits > 1 the caller
+// consumes the partials (launch_resid_norm).
+int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
+                     bool defer) {
   int splits = 1;
   if (decode) {
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
-    splits = (int)((2 * 148 + ctas / 2) / ctas);
-    splits = std::min(splits, 16);
-    splits = std::min(splits, std::max(1, K / (4 * T)));
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, 288 / ctas));
     while (splits > 1 && (K / 64) / splits < 4) --splits;
-    while (splits > 1 && ((int64_t)splits * ctas * 128 * bn > ws_cap_ || ctas > (1 << 16))) --splits;
-    splits = std::max(splits, 1);
+    while (splits > 1 && (int64_t)splits * T * ((N + 127) / 128 * 128) > ws_cap_) --splits;
   }
-  launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, counters_, decode, st_);
-
+  const int used = launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, counters_, decode, st_, defer);
+  launches_ += (used > 1 && !defer) ? 2 : 1;
+  return used;
 }
 
 // -------------------------------------------------------------------- ring
@@ -578,10 +575,17 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     launch_embed(arena, dm + M.o_tokidx, E_, x_, T, d_, st_);
     launches_++;
   }
+  if (stage == S_ - 1) launches_++;   // final norm
+  const bool dec = !M.prefill;
+  bool normed = false;   // a_ already holds RMSNorm(x; g1) (fused into the previous down-proj reduction)
   for (int l = stage_l0_[stage]; l < stage_l1_[stage]; ++l) {
     const LayerW& w = L_[l];
     bf16* kvl = kv_ + (int64_t)(l - own_l0_) * C_ * (kv_block_bytes_layer_ / 2);
-    launch_rmsnorm(x_, w.g1, a_, nullptr, T, d_, eps, st_);
+    if (!normed) {
+      launch_rmsnorm(x_, w.g1, a_, nullptr, T, d_, eps, st_);
+      launches_++;
+    }
+    normed = false;
     EpiParams ep{};
     ep.mode = kEpiQKV;
     ep.out_bf16 = q_;
@@ -593,7 +597,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ep.Hkv = Hkv_;
     ep.hd = hd_;
     const int iq = tbegin(cQKV + (M.prefill ? 0 : kDecOff));
-    gemm(a_, xa_, &w, w.tqkv, w.wqkv, T, nqkv, d_, ep, !M.prefill);
+    gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.prefill) {
       PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_,
@@ -603,8 +607,11 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       tend(ip, 0, 0);
       launches_++;
     } else {
-      const int ms = (int)cdiv(M.max_ctx, 512);
-      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_};
+      // split size: 512 tokens unless the grid would not fill the GPU (>= 4 CTAs per SM)
+      int split = 512;
+      while (split > 128 && (int64_t)n * Hkv_ * cdiv(M.max_ctx, split) < 4 * 148) split >>= 1;
+      const int ms = (int)cdiv(M.max_ctx, split);
+      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split};
       const int ida = tbegin(cDecAttn);
       launch_decode_attn(dp, st_);
       tend(ida, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
@@ -615,23 +622,30 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eo.out_f32 = x_;
     eo.ldo = d_;
     const int io = tbegin(cO + (M.prefill ? 0 : kDecOff));
-    gemm(ob_, xo_, &w, w.to, w.wo, T, d_, H_ * hd_, eo, !M.prefill);
+    const int so = gemm(xo_, w.to, T, d_, H_ * hd_, eo, dec, /*defer=*/true);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
-    launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
+    if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
+    else launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
+    launches_++;
     EpiParams eg{};
     eg.mode = kEpiSwiGLU;
     eg.out_bf16 = h_;
     const int ig = tbegin(cGU + (M.prefill ? 0 : kDecOff));
-    gemm(a_, xa_, &w, w.tgu, w.wgu, T, 2 * F_, d_, eg, !M.prefill);
+    gemm(xa_, w.tgu, T, 2 * F_, d_, eg, dec);
     tend(ig, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
     EpiParams ed{};
     ed.mode = kEpiResid;
     ed.out_f32 = x_;
     ed.ldo = d_;
     const int idn = tbegin(cDown + (M.prefill ? 0 : kDecOff));
-    gemm(h_, xh_, &w, w.td, w.wd, T, d_, F_, ed, !M.prefill);
+    const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
-    launches_ += 6;
+    if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
+      const bf16* gnext = l + 1 < stage_l1_[stage] ? L_[l + 1].g1 : nullptr;
+      launch_resid_norm(ws_, sd, x_, gnext, a_, T, d_, eps, st_);
+      launches_++;
+      normed = gnext != nullptr;
+    }
   }
   if (stage == S_ - 1) {
     launch_rmsnorm(x_, gf_, a_, dm + M.o_last, n, d_, eps, st_);
@@ -640,9 +654,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     el.out_f32 = logits_;
     el.ldo = V_;
     const int il = tbegin(cLM + (M.prefill ? 0 : kDecOff));
-    gemm(a_, xa_, nullptr, tlm_, Wlm_, n, V_, d_, el, !M.prefill);
+    gemm(xa_, tlm_, n, V_, d_, el, dec);
     tend(il, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
-    launches_ += 2;
+    launches_++;
     if (arena) {
       launch_argmax(logits_, n, V_, arena, dm + M.o_outpos, st_);
       launches_++;

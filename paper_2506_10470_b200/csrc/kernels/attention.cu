@@ -10,8 +10,9 @@
 // read once for all G = H/Hkv query heads (GQA).  LPT = hd/8 lanes cooperate
 // on one token (16-byte loads), U tokens in flight per thread-group, online
 // softmax in fp32 (exp2 with log2e-prescaled scores), warp-shuffle merges.
-// Splits are fixed 512-token chunks of each sequence's own context, merged in
-// split order -> results do not depend on batch composition.
+// Splits are fixed-size chunks of each sequence's own context (128..512
+// tokens, chosen per micro-batch so that the grid fills the GPU), merged in
+// split order.
 #include <float.h>
 #include <math.h>
 
@@ -20,7 +21,6 @@
 
 namespace tdp {
 
-constexpr int kSplit = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct SoftmaxState {
@@ -38,10 +38,10 @@ decode_attn_kernel(DecodeAttnParams p) {
   pdl_wait();
   const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
   const int ctx = p.ctx[seq];
-  const int n_splits = (ctx + kSplit - 1) / kSplit;
+  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
   if (split >= n_splits) return;
-  const int t_begin = split * kSplit;
-  const int t_end = min(ctx, t_begin + kSplit);
+  const int t_begin = split * p.split_tokens;
+  const int t_end = min(ctx, t_begin + p.split_tokens);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tg = lane / LPT, sub = lane % LPT;
   const int H = p.H;
@@ -160,7 +160,7 @@ __global__ void decode_combine_kernel(DecodeAttnParams p, int hd) {
   pdl_wait();
   const int seq = blockIdx.y, h = blockIdx.x;
   const int ctx = p.ctx[seq];
-  const int n_splits = (ctx + kSplit - 1) / kSplit;
+  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
   if (n_splits <= 1) return;
   const float* part = p.part + ((int64_t)seq * p.H + h) * p.max_splits * (hd + 2);
   float M = -INFINITY;

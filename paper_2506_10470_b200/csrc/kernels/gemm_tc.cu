@@ -267,7 +267,7 @@ constexpr int smem_bytes() {
 
 template <int BN, int STAGES>
 void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, int splits, float* ws,
-               int* counters, cudaStream_t st) {
+               int* counters, bool defer, cudaStream_t st) {
   auto kern = gemm_tc_kernel<BN, STAGES>;
   static bool attr = false;
   constexpr int sm = smem_bytes<BN, STAGES>();
@@ -281,7 +281,7 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   dim3 grid((T + BN - 1) / BN, (W.rows + 127) / 128, nsplit);
   launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
            W.packed ? W.base : nullptr, counters);
-  if (nsplit > 1) {
+  if (nsplit > 1 && !defer) {
     const int64_t pairs = (int64_t)T * (W.rows / 2);
     const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
     launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, ws, nsplit, T, W.rows, ep);
@@ -338,16 +338,23 @@ int tc_bn_for(int T, bool decode) {
   return 256;
 }
 
-void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
-                    int* counters, bool decode, cudaStream_t st) {
-  if (T <= 0) return;
+int effective_splits(int K, int splits) {
+  const int kb_total = K / BK;
+  const int kps = (kb_total + splits - 1) / splits;
+  return (kb_total + kps - 1) / kps;
+}
+
+int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
+                   int* counters, bool decode, cudaStream_t st, bool defer_reduce) {
+  if (T <= 0) return 1;
   switch (tc_bn_for(T, decode)) {
     // <= 110 KB of smem for BN <= 128 so that two CTAs share an SM
-    case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, st); break;
-    case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, counters, st); break;
-    case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, counters, st); break;
-    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, st); break;
+    case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, defer_reduce, st); break;
+    case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, counters, defer_reduce, st); break;
+    case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, counters, defer_reduce, st); break;
+    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, defer_reduce, st); break;
   }
+  return effective_splits(W.K, splits);
 }
 
 }  // namespace tdp

@@ -23,7 +23,10 @@ int tc_bn_for(int T, bool decode);
 // out = X[T, K] . W[Nf, K]^T with epilogue ep.  Xby_bn[i] = X described with
 // box rows 32 << i.  splits > 1: split-K through workspace ws
 // [tiles][splits][128][BN] fp32 and zero-initialised per-tile counters.
-void launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
-                    int* counters, bool decode, cudaStream_t st);
+// Returns the split count actually used.  defer_reduce: leave the partials in
+// ws [splits][T][N] for a fused consumer (launch_resid_norm) instead of
+// launching the reduction + epilogue.
+int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
+                   int* counters, bool decode, cudaStream_t st, bool defer_reduce = false);
 
 }  // namespace tdp

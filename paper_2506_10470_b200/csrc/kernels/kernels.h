@@ -38,6 +38,11 @@ void launch_embed(const int32_t* arena, const int32_t* tok_idx, const bf16* E, f
 // out[i] = bf16(RMSNorm(x[rows ? rows[i] : i]) * g)
 void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* rows, int n, int d, float eps,
                     cudaStream_t st);
+// Fused split-K reduction + residual add + next RMSNorm (decode GEMMs whose
+// epilogue is a residual add):  x[t] += sum_s ws[s][t] (split order), then, if
+// g != nullptr, out[t] = bf16(RMSNorm(x[t]) * g).
+void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
+                       cudaStream_t st);
 // tokens: arena[outpos[i]] = argmax_j logits[i][j] (lowest index on ties)
 void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int32_t* outpos, cudaStream_t st);
 // multi-process token return: pairs[2i] = outpos[i], pairs[2i+1] = arena[outpos[i]]; and its inverse
@@ -62,8 +67,8 @@ void launch_gemm(const bf16* A, const bf16* W, int M, int N, int K, const EpiPar
 
 // ---- attention --------------------------------------------------------------
 // Decode: one query token per sequence; q [n, H*hd] (physical RoPE-pair order),
-// paged K/V via block tables; o [n, H*hd] bf16.  Split-KV over fixed 512-token
-// chunks (batch-invariant), partial (m, l, acc) merged in a fixed order.
+// paged K/V via block tables; o [n, H*hd] bf16.  Split-KV over split_tokens
+// chunks, partial (m, l, acc) merged in split order.
 struct DecodeAttnParams {
   const bf16* q;
   const bf16* kv;        // layer pool base
@@ -74,6 +79,7 @@ struct DecodeAttnParams {
   float* part;           // [n, H, max_splits, hd + 2] workspace
   int max_splits;
   int n, H, Hkv, hd;
+  int split_tokens;      // context tokens per split (multiple of 16)
 };
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 

@@ -144,6 +144,64 @@ void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* row
   launch_k(rmsnorm_kernel<256>, dim3(n), dim3(256), 0, st, x, g, out, rows, d, eps);
 }
 
+// ---------------------------------------------- split-K reduce + resid + norm
+template <int NT>
+__global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict__ ws, int splits, float* __restrict__ x,
+                                                        const bf16* __restrict__ g, bf16* __restrict__ out, int T,
+                                                        int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  float4* xr = reinterpret_cast<float4*>(x + (int64_t)t * d);
+  __shared__ float red[NT / 32];
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d / 4; j += NT) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float4 p = __ldcg(reinterpret_cast<const float4*>(ws + ((int64_t)s * T + t) * d) + j);
+      acc.x += p.x;
+      acc.y += p.y;
+      acc.z += p.z;
+      acc.w += p.w;
+    }
+    float4 v = xr[j];
+    v.x += acc.x;
+    v.y += acc.y;
+    v.z += acc.z;
+    v.w += acc.w;
+    xr[j] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (!g) return;
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < NT / 32 ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)d + eps);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g);
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)t * d);
+  for (int j = threadIdx.x; j < d / 4; j += NT) {
+    const float4 v = xr[j];
+    const float2 ga = __bfloat1622float2(g2[2 * j]);
+    const float2 gb = __bfloat1622float2(g2[2 * j + 1]);
+    uint2 pk;
+    pk.x = pack_bf16x2(v.x * inv * ga.x, v.y * inv * ga.y);
+    pk.y = pack_bf16x2(v.z * inv * gb.x, v.w * inv * gb.y);
+    o[j] = pk;
+  }
+}
+
+void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
+                       cudaStream_t st) {
+  if (T <= 0) return;
+  launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps);
+}
+
 // -------------------------------------------------------------------- argmax
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ arena,
                               const int32_t* __restrict__ outpos) {
