@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -70,6 +72,27 @@ TDP_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar
       : "memory");
 }
 TDP_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+TDP_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+TDP_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+TDP_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+TDP_DEV void umma_commit_mc(uint64_t* b, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(b)),
+               "h"(mask)
+               : "memory");
+}
 TDP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 TDP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 TDP_DEV void umma_commit(uint64_t* b) {
@@ -105,7 +128,11 @@ TDP_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN, int STAGES>
+// CM > 1: a cluster of CM CTAs along the weight-row dimension shares one
+// token tile; each CTA TMA-loads BN/CM token rows and multicasts them to the
+// whole cluster (cuts L2->SM traffic for the compute-bound prefill GEMMs);
+// every CTA's MMA completion frees the stage in all CTAs (multicast commit).
+template <int BN, int STAGES, int CM>
 __global__ void __launch_bounds__(192, BN <= 128 ? 2 : 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Nf, int T,
                int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws, const bf16* __restrict__ wpk,
@@ -135,7 +162,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CM);
     }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -148,9 +175,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CM > 1) cluster_sync_all();   // peers' barriers exist before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t crank = CM > 1 ? cluster_ctarank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << CM) - 1);
+  constexpr int XS = BN / CM;                 // token rows this CTA loads (and multicasts)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -170,8 +201,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         load_w(sa, kb0 + i, &full[i]);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_2d(smem + i * STAGE_BYTES + A_BYTES, &tmX, (kb0 + i) * BK, n0, &full[i]);
+      auto load_x = [&](uint8_t* dst, int kb, uint64_t* bar) {
+        if constexpr (CM == 1) tma_load_2d(dst, &tmX, kb * BK, n0, bar);
+        else tma_load_2d_mc(dst + crank * XS * 128, &tmX, kb * BK, n0 + (int)crank * XS, bar, kMask);
+      };
+      for (int i = 0; i < pre; ++i) load_x(smem + i * STAGE_BYTES + A_BYTES, kb0 + i, &full[i]);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
@@ -179,7 +213,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         uint8_t* sa = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
         load_w(sa, kb0 + i, &full[s]);
-        tma_load_2d(sa + A_BYTES, &tmX, (kb0 + i) * BK, n0, &full[s]);
+        load_x(sa + A_BYTES, kb0 + i, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -199,7 +233,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)   // advance 16 elements = 32 B inside the swizzle atom
           umma_f16(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
-        umma_commit(&empty[s]);
+        if constexpr (CM > 1) umma_commit_mc(&empty[s], kMask);
+        else umma_commit(&empty[s]);
       }
       umma_commit(accf);
     }
@@ -234,7 +269,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     }
     tc_fence_before();
   }
-  __syncthreads();
+  if constexpr (CM > 1) cluster_sync_all();   // no CTA leaves while peers may still signal it
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
@@ -265,10 +301,10 @@ constexpr int smem_bytes() {
   return STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;   // + alignment + barriers
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CM = 1>
 void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, int splits, float* ws,
                int* counters, bool defer, cudaStream_t st) {
-  auto kern = gemm_tc_kernel<BN, STAGES>;
+  auto kern = gemm_tc_kernel<BN, STAGES, CM>;
   static bool attr = false;
   constexpr int sm = smem_bytes<BN, STAGES>();
   if (!attr) {
@@ -279,8 +315,12 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   const int kps = (kb_total + splits - 1) / splits;
   const int nsplit = (kb_total + kps - 1) / kps;
   dim3 grid((T + BN - 1) / BN, (W.rows + 127) / 128, nsplit);
-  launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
-           W.packed ? W.base : nullptr, counters);
+  if constexpr (CM > 1)
+    launch_kc(kern, grid, dim3(192), sm, st, CM, W.map, X.map, W.rows, T, kps, kb_total, ep,
+              nsplit > 1 ? ws : nullptr, W.packed ? W.base : nullptr, counters);
+  else
+    launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
+             W.packed ? W.base : nullptr, counters);
   if (nsplit > 1 && !defer) {
     const int64_t pairs = (int64_t)T * (W.rows / 2);
     const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
@@ -338,6 +378,16 @@ int tc_bn_for(int T, bool decode) {
   return 256;
 }
 
+// TDPIPE_MC=0 disables the cluster-multicast prefill path (A/B measurements)
+static bool mc_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TDPIPE_MC");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int effective_splits(int K, int splits) {
   const int kb_total = K / BK;
   const int kps = (kb_total + splits - 1) / splits;
@@ -352,7 +402,17 @@ int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const Epi
     case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, defer_reduce, st); break;
     case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, counters, defer_reduce, st); break;
     case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, counters, defer_reduce, st); break;
-    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, defer_reduce, st); break;
+    default: {
+      // prefill: cluster the weight-row tiles and multicast the 256-token tile
+      const int mt = (W.rows + 127) / 128;
+      if (mc_enabled() && mt % 4 == 0 && splits <= 1)
+        launch_bn<256, 4, 4>(W, Xby_bn[1], T, ep, 1, ws, counters, defer_reduce, st);
+      else if (mc_enabled() && mt % 2 == 0 && splits <= 1)
+        launch_bn<256, 4, 2>(W, Xby_bn[2], T, ep, 1, ws, counters, defer_reduce, st);
+      else
+        launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, defer_reduce, st);
+      break;
+    }
   }
   return effective_splits(W.K, splits);
 }
