@@ -18,6 +18,7 @@ ap.add_argument("--ctx", type=int, default=300)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--model", default="llama2_7b")
 ap.add_argument("--no-prefill", action="store_true")
+ap.add_argument("--prefill-only", action="store_true")
 a = ap.parse_args()
 shape = SHAPES[a.model].with_layers(a.layers)
 t = TDPipe(shape, 1, kv_blocks=a.b * ((a.ctx + a.steps + 15) // 16 + 1) + 16)
@@ -29,7 +30,7 @@ for s in (range(0, a.b, per) if not a.no_prefill else []):
     idx = list(range(s, min(a.b, s + per)))
     toks = rng.integers(0, shape.vocab, size=a.ctx * len(idx)).astype(np.int32)
     t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * len(idx), [a.ctx] * len(idx), bt[idx], toks)
-for step in range(a.steps):
+for step in (range(a.steps) if not a.prefill_only else []):
     toks = rng.integers(0, shape.vocab, size=a.b).astype(np.int32)
     t.td_stage_forward(0, TD_BATCH_DECODE, [a.ctx + step] * a.b, [1] * a.b, bt, toks)
 print("done")
