@@ -63,4 +63,87 @@ TDP_DEV void epilogue_pair(const EpiParams& ep, int M, int N, int m, int n, floa
   }
 }
 
+// Swap-AB tcgen05 epilogue for one 32-token chunk: this lane owns output
+// feature f and holds its accumulators for tokens t0 .. t0+31 in r[].  Per-token
+// metadata (position, KV slot) is loaded once per chunk by lane j for token
+// t0+j and broadcast with shuffles; all other loads of a chunk are issued
+// before any store, so the chunk costs one memory latency instead of 32.
+// Every lane executes the shuffles (no divergence around them).
+TDP_DEV void epilogue_chunk(const EpiParams& ep, int T, int Nf, int f, int t0, const uint32_t* r) {
+  const int lane = threadIdx.x & 31;
+  const bool even = (lane & 1) == 0;
+  const bool fok = f < Nf;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  switch (ep.mode) {
+    case kEpiF32: {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (t0 + j < T && fok) ep.out_f32[(int64_t)(t0 + j) * ep.ldo + f] = v[j];
+      break;
+    }
+    case kEpiResid: {
+      float xo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        xo[j] = (t0 + j < T && fok) ? ep.out_f32[(int64_t)(t0 + j) * ep.ldo + f] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (t0 + j < T && fok) ep.out_f32[(int64_t)(t0 + j) * ep.ldo + f] = xo[j] + v[j];
+      break;
+    }
+    case kEpiSwiGLU: {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float u = __shfl_xor_sync(0xffffffffu, v[j], 1);
+        if (even && t0 + j < T && fok) ep.out_bf16[(int64_t)(t0 + j) * (Nf >> 1) + (f >> 1)] = __float2bfloat16_rn(silu(v[j]) * u);
+      }
+      break;
+    }
+    case kEpiBF16: {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (t0 + j < T && fok) ep.out_bf16[(int64_t)(t0 + j) * ep.ldo + f] = __float2bfloat16_rn(v[j]);
+      break;
+    }
+    case kEpiQKV: {
+      const int hd = ep.hd, half = hd >> 1;
+      const int qcols = ep.H * hd, kcols = ep.Hkv * hd;
+      const int tl = t0 + lane;
+      const int my_pos = tl < T ? ep.pos[tl] : 0;
+      const int my_slot = tl < T ? ep.slot[tl] : 0;
+      const bool rot = f < qcols + kcols;
+      const int i = (f % hd) >> 1;
+      float2 cs[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int pj = __shfl_sync(0xffffffffu, my_pos, j);
+        cs[j] = (rot && fok && t0 + j < T) ? *reinterpret_cast<const float2*>(ep.rope_cs + ((int64_t)pj * half + i) * 2)
+                                           : make_float2(1.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float pv = __shfl_xor_sync(0xffffffffu, v[j], 1);
+        const int sj = __shfl_sync(0xffffffffu, my_slot, j);
+        const int t = t0 + j;
+        if (t >= T || !fok) continue;
+        // rotate-half pair (x_e, x_o) = (lane even, lane odd)
+        const float out = !rot ? v[j] : (even ? v[j] * cs[j].x - pv * cs[j].y : v[j] * cs[j].x + pv * cs[j].y);
+        const bf16 ob = __float2bfloat16_rn(out);
+        if (f < qcols) {
+          ep.out_bf16[(int64_t)t * qcols + f] = ob;
+        } else if (f < qcols + kcols) {
+          const int kn = f - qcols;
+          ep.kcache[((((int64_t)(sj >> 4) * 2 + 0) * ep.Hkv + kn / hd) * kBlock + (sj & 15)) * hd + kn % hd] = ob;
+        } else {
+          const int vn = f - qcols - kcols;
+          ep.kcache[((((int64_t)(sj >> 4) * 2 + 1) * ep.Hkv + vn / hd) * kBlock + (sj & 15)) * hd + vn % hd] = ob;
+        }
+      }
+      break;
+    }
+  }
+}
+
 }  // namespace tdp

@@ -245,7 +245,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     tc_fence_after();
     const int q = warp & 3;
     const int f = m0 + q * 32 + lane;            // this lane's output feature
-    const bool even = (lane & 1) == 0;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
@@ -258,13 +257,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           if (t < T && f < Nf) __stcg(ws + ((int64_t)blockIdx.z * T + t) * Nf + f, __uint_as_float(r[j]));
         }
       } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float v = __uint_as_float(r[j]);
-          const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
-          const int t = n0 + c + j;
-          if (even && t < T) epilogue_pair(ep, T, Nf, t, f, v, vp);
-        }
+        epilogue_chunk(ep, T, Nf, f, n0 + c, r);
       }
     }
     tc_fence_before();

@@ -1,0 +1,15 @@
+"""Prefill GEMM throughput (T = 2048) for the Llama-2-7B shapes."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_10470_b200.tdpipe import td_bench_gemm  # noqa: E402
+
+shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gu": (22016, 4096), "down": (4096, 11008)}
+for T in [2048, 1024]:
+    for name, (N, K) in shapes.items():
+        us = td_bench_gemm(T, N, K, 1, False, iters=20, copies=2)
+        tf = 2.0 * T * N * K / (us * 1e-6) / 1e12
+        print(json.dumps(dict(T=T, gemm=name, mc=os.environ.get("TDPIPE_MC", "1"), us=round(us, 1), TFLOPs=round(tf, 1),
+                              frac_sustained=round(tf / 1406.7, 3))), flush=True)
