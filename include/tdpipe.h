@@ -86,6 +86,9 @@ typedef struct td_options {
   int32_t world_size;           /* 1 = single process                                  */
   int32_t rank;                 /* this process's stage                                */
   const void* nccl_ids;         /* 2 x 128-byte ncclUniqueId (fwd, bwd) from td_nccl_ids */
+  /* ablations of the paper's §4.4 (0 = the paper's method) */
+  int32_t p2d_kv_permille;      /* P->D once allocated KV >= x/1000 of C */
+  int32_t d2p_finish_permille;  /* D->P once x/1000 of the decode cohort finished */
 } td_options;
 
 typedef struct td_run_stats {

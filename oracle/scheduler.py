@@ -52,6 +52,9 @@ class SchedOptions:
     steal: int = 1
     alg1_check_before_launch: int = 0   # [R11b] verbatim = 0 (launch precedes check)
     eq2_bubble_scale: int = 1           # sigma [R12b]; 1 = verbatim Eq.2
+    # ablations (§4.4.1, 660-662 §4.4.3); 0 = the paper's method
+    p2d_kv_permille: int = 0            # switch to decode once allocated KV >= ratio * C
+    d2p_finish_permille: int = 0        # switch to prefill once this fraction of the decode cohort finished
 
 
 @dataclass
@@ -149,6 +152,8 @@ class RefScheduler:
         self.adm_counter = 0
         self.mb_counter = 0
         self.stats = dict(p2d=0, d2p=0, stolen=0, evicted=0, refilled=0)
+        self.cohort_n = 0          # requests of the current decode phase (ablation A23)
+        self.cohort_done = 0
         n = len(self.reqs)
         # futurePoints: s, 2s, ..., H, H >= every remaining length [R3]
         s = opts.fp_stride
@@ -275,7 +280,12 @@ class RefScheduler:
             launched += 1
             for rid in batch:                    # foreach request: UpdateUsage
                 self.update_usage(U, self.reqs[rid])
-            if self.check_switch(U, self.C):     # CheckSwitch
+            if self.o.p2d_kv_permille:
+                # ablation: "switch to decode once <ratio> of the KV cache blocks are occupied"
+                if (self.C - self.alloc.free) * 1000 >= self.o.p2d_kv_permille * self.C:
+                    reason = "kv_ratio"
+                    break
+            elif self.check_switch(U, self.C):   # CheckSwitch
                 reason = "forecast"
                 break
         self.stats["p2d"] += 1
@@ -306,7 +316,10 @@ class RefScheduler:
                 for fp in self.fps:
                     if fp <= rem:
                         U[fp] += ceil_div(r.L + fp, self.B)
-            if self.check_switch(U, self.C):
+            if self.o.p2d_kv_permille:
+                if (self.C - free) * 1000 >= self.o.p2d_kv_permille * self.C:
+                    break
+            elif self.check_switch(U, self.C):
                 break
         return ks
 
@@ -339,6 +352,8 @@ class RefScheduler:
         self.epoch += 1
         self.pool.clear()
         members = sorted(self.live, key=lambda i: self.reqs[i].adm)
+        self.cohort_n = len(members)
+        self.cohort_done = 0
         for r in self.reqs:
             r.slot = -1
         self.slots = []
@@ -480,6 +495,12 @@ class RefScheduler:
         ks = self.dry_run_prefill()
         if not ks:
             return False
+        if self.o.d2p_finish_permille:
+            # ablation: switch "once <ratio> of the requests have completed"
+            if self.cohort_done * 1000 >= self.o.d2p_finish_permille * self.cohort_n:
+                self.emit("S", "D2P", "finish_ratio", self.cohort_done, self.cohort_n)
+                return True
+            return False
         bs = len(sl.members)
         tpre = [self._tpre(k) for k in ks]
         if bs == 0:
@@ -498,6 +519,7 @@ class RefScheduler:
     # ------------------------------------------------------------ S6 returns
     def finish(self, r: Req) -> None:
         r.done = True
+        self.cohort_done += 1
         self.alloc.release(r.blocks)
         self.emit("F", r.rid, *r.blocks)
         r.blocks = []

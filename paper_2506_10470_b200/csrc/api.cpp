@@ -64,6 +64,8 @@ extern "C" void td_default_options(td_options* o) {
   o->world_size = 1;
   o->rank = 0;
   o->nccl_ids = nullptr;
+  o->p2d_kv_permille = 0;
+  o->d2p_finish_permille = 0;
 }
 
 static bool read_profile(const std::string& path, std::vector<int64_t>* tdec, std::vector<int64_t>* tpre,
@@ -176,6 +178,8 @@ extern "C" td_status td_run(td_ctx* c, td_run_stats* st) {
   so.steal = c->opt.steal;
   so.check_before_launch = c->opt.alg1_check_before_launch;
   so.eq2_bubble_scale = c->opt.eq2_bubble_scale;
+  so.p2d_kv_permille = c->opt.p2d_kv_permille;
+  so.d2p_finish_permille = c->opt.d2p_finish_permille;
   if (so.policy == TD_POLICY_TDPIPE && c->tdec.size() < 2 && c->reqs.size() > 0) {
     // without a profile table Eq.1/Eq.2 cannot be evaluated: use a flat one
     // (never switches before the queue drains is NOT implied; document it)

@@ -154,7 +154,12 @@ int Controller::prefill_phase() {
     if (int rc = launch_prefill(batch, -1)) return rc;      // getPrefillBatch().Launch()
     ++launched;
     for (int rid : batch) update_usage(U, reqs_[rid]);     // UpdateUsage per request
-    if (check_switch(U)) { reason = "forecast"; break; }   // CheckSwitch
+    if (opt_.p2d_kv_permille) {                            // ablation: KV occupancy ratio
+      if ((opt_.C - free_blocks()) * 1000 >= (int64_t)opt_.p2d_kv_permille * opt_.C) { reason = "kv_ratio"; break; }
+    } else if (check_switch(U)) {                          // CheckSwitch
+      reason = "forecast";
+      break;
+    }
   }
   stats_.p2d++;
   char buf[128];
@@ -185,7 +190,11 @@ std::vector<int64_t> Controller::dry_run_prefill() const {
     ks.push_back(k);
     ++launched;
     add_usage_fresh(U, batch);
-    if (check_switch(U)) break;
+    if (opt_.p2d_kv_permille) {
+      if ((opt_.C - free) * 1000 >= (int64_t)opt_.p2d_kv_permille * opt_.C) break;
+    } else if (check_switch(U)) {
+      break;
+    }
   }
   return ks;
 }
@@ -230,6 +239,8 @@ void Controller::form_decode() {
   pool_.clear();
   std::vector<int> members(live_.begin(), live_.end());
   std::sort(members.begin(), members.end(), [&](int a, int b) { return reqs_[a].adm < reqs_[b].adm; });
+  cohort_n_ = (int64_t)members.size();
+  cohort_done_ = 0;
   for (auto& r : reqs_) r.slot = -1;
   slots_.clear();
   const int n = (int)members.size();
@@ -397,6 +408,13 @@ void Controller::steal_refill(Slot& sl) {
 bool Controller::decide_switch(Slot& sl) {
   std::vector<int64_t> ks = dry_run_prefill();
   if (ks.empty()) return false;
+  if (opt_.d2p_finish_permille) {   // ablation: request-finish ratio of the decode cohort
+    if (cohort_done_ * 1000 >= (int64_t)opt_.d2p_finish_permille * cohort_n_) {
+      emit_ids("S D2P finish_ratio", {cohort_done_, cohort_n_});
+      return true;
+    }
+    return false;
+  }
   const int64_t bs = (int64_t)sl.members.size();
   int64_t sum_pre = 0, max_pre = 0;
   for (int64_t k : ks) { const int64_t t = tpre(k); sum_pre += t; max_pre = std::max(max_pre, t); }
@@ -421,6 +439,7 @@ bool Controller::decide_switch(Slot& sl) {
 // ------------------------------------------------------------ S6 returns
 void Controller::finish(Req& r) {
   r.done = true;
+  cohort_done_++;
   release(r.blocks);
   std::vector<int64_t> line{r.rid};
   for (int32_t b : r.blocks) line.push_back(b);

@@ -38,6 +38,8 @@ struct SchedOptions {
   int steal = 1;
   int check_before_launch = 0;
   int eq2_bubble_scale = 1;
+  int p2d_kv_permille = 0;      // ablation A22: KV-occupancy-ratio P->D switch
+  int d2p_finish_permille = 0;  // ablation A23: request-finish-ratio D->P switch
 };
 
 struct Req {
@@ -152,6 +154,7 @@ class Controller {
   int64_t mb_counter_ = 0;
   std::vector<int> fps_;
   int64_t ctx_rep_ = 1, b_mem_ = 1, Bp_ = 1;
+  int64_t cohort_n_ = 0, cohort_done_ = 0;
   ExecHooks* ex_ = nullptr;
   SchedStats stats_;
 };

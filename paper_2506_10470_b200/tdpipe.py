@@ -35,7 +35,8 @@ class td_options(C.Structure):
                 ("steal", C.c_int32), ("alg1_check_before_launch", C.c_int32),
                 ("eq2_bubble_scale", C.c_int32), ("weight_seed", C.c_uint64),
                 ("profile_csv", C.c_char_p), ("log_decisions", C.c_int32), ("record_logits", C.c_int32),
-                ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_ids", C.c_void_p)]
+                ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_ids", C.c_void_p),
+                ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32)]
 
 
 class td_run_stats(C.Structure):

@@ -24,13 +24,15 @@ def _run_both(wl, tmp_path, tag, **o):
     so = SchedOptions(n_stages=o["W"], block_size=o["B"], kv_blocks=o["C"], prefill_token_budget=o["budget"],
                       max_batch_seqs=o["max_seqs"], fp_stride=o["stride"], fp_horizon=o["horizon"],
                       policy=o["policy"], steal=o["steal"], alg1_check_before_launch=o["cbl"],
-                      eq2_bubble_scale=o["sigma"])
+                      eq2_bubble_scale=o["sigma"], p2d_kv_permille=o.get("kvp", 0),
+                      d2p_finish_permille=o.get("finp", 0))
     ref = schedule(reqs, so, tdec, tpre)
     shape = dataclasses.replace(SHAPES["tiny"].with_layers(max(2, o["W"])), max_seq_len=4096)
     t = TDPipe(shape, o["W"], executor=TD_EXEC_NULL, block_size=o["B"], kv_blocks=o["C"],
                prefill_token_budget=o["budget"], max_batch_seqs=o["max_seqs"], fp_stride=o["stride"],
                fp_horizon=o["horizon"], policy=o["policy"], steal=o["steal"], alg1_check_before_launch=o["cbl"],
-               eq2_bubble_scale=o["sigma"], profile_csv=csv)
+               eq2_bubble_scale=o["sigma"], profile_csv=csv, p2d_kv_permille=o.get("kvp", 0),
+               d2p_finish_permille=o.get("finp", 0))
     t.submit_workload(wl)
     st = t.td_run()
     got = t.td_get_log()
@@ -55,7 +57,8 @@ def test_parity_random_tiny_workloads(tmp_path):
                  stride=int(rng.choice([1, 2, 4, 32])), horizon=int(rng.choice([4, 16, 64])), policy=policy,
                  steal=int(rng.integers(0, 2)), cbl=int(rng.integers(0, 2)), sigma=int(rng.choice([1, max(1, W - 1)])),
                  tables=synthetic_profile(int(rng.choice([8, 64])), int(rng.choice([32, 512])),
-                                          knee=int(rng.integers(0, 12))))
+                                          knee=int(rng.integers(0, 12))),
+                 kvp=int(rng.choice([0, 0, 0, 300, 700])), finp=int(rng.choice([0, 0, 0, 250, 500, 900])))
         got, want, st, ref, n_out = _run_both(wl, tmp_path, seed % 7, **o)
         assert got == want, f"seed {seed} opts {o}\n--- first diff at line " + str(
             next((i for i, (a, b) in enumerate(zip(got.splitlines(), want.splitlines())) if a != b), None))
