@@ -371,12 +371,14 @@ int tc_bn_for(int T, bool decode) {
   return 256;
 }
 
-// TDPIPE_MC=0 disables the cluster-multicast prefill path (A/B measurements)
+// TDPIPE_MC=1 enables the cluster-multicast prefill path.  Off by default: the
+// measured sweep (profiles/r1) shows the single-CTA path at 94-106% of the
+// sustained bf16 peak and the multicast variant 5-15% slower.
 static bool mc_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = std::getenv("TDPIPE_MC");
-    on = (e && e[0] == '0') ? 0 : 1;
+    on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }
