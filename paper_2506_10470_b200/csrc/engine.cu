@@ -68,6 +68,7 @@ struct Meta {
 struct TimedLaunch {
   cudaEvent_t a, b;
   int cls;
+  int sub = -1;     // optional second class (batch-size bucket)
   double bytes, flops;
 };
 
@@ -186,12 +187,17 @@ class CudaEngine : public Engine {
   std::map<std::string, KernelTiming> timing_acc_;
   std::vector<std::string> cls_names_{"decode_attn", "prefill_attn", "gemm_qkv_pre", "gemm_o_pre", "gemm_gu_pre",
                                       "gemm_down_pre", "lm_head_pre", "norm", "stage", "mb", "gemm_qkv_dec",
-                                      "gemm_o_dec", "gemm_gu_dec", "gemm_down_dec", "lm_head_dec"};
+                                      "gemm_o_dec", "gemm_gu_dec", "gemm_down_dec", "lm_head_dec",
+                                      "decode_attn@b1-8", "decode_attn@b9-32", "decode_attn@b33-128",
+                                      "decode_attn@b129+", "gemm_dec@b1-8", "gemm_dec@b9-32", "gemm_dec@b33-128",
+                                      "gemm_dec@b129+"};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev_;
 };
 
 enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
 constexpr int kDecOff = 8;   // decode-phase GEMM classes = prefill class + kDecOff
+constexpr int kAttnBucket = 15, kGemmBucket = 19;   // + bucket(n): batch-size buckets for decode
+static inline int bucket_of(int n) { return n <= 8 ? 0 : n <= 32 ? 1 : n <= 128 ? 2 : 3; }
 
 // --------------------------------------------------------------------- init
 td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_options& o) {
@@ -597,6 +603,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ep.Hkv = Hkv_;
     ep.hd = hd_;
     const int iq = tbegin(cQKV + (M.prefill ? 0 : kDecOff));
+    if (iq >= 0 && !M.prefill) timed_[iq].sub = kGemmBucket + bucket_of(T);
     gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.prefill) {
@@ -613,6 +620,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       const int ms = (int)cdiv(M.max_ctx, split);
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split};
       const int ida = tbegin(cDecAttn);
+      if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
       launch_decode_attn(dp, st_);
       tend(ida, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
       launches_ += ms > 1 ? 2 : 1;
@@ -622,6 +630,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eo.out_f32 = x_;
     eo.ldo = d_;
     const int io = tbegin(cO + (M.prefill ? 0 : kDecOff));
+    if (io >= 0 && !M.prefill) timed_[io].sub = kGemmBucket + bucket_of(T);
     const int so = gemm(xo_, w.to, T, d_, H_ * hd_, eo, dec, /*defer=*/true);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
     if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
@@ -631,6 +640,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eg.mode = kEpiSwiGLU;
     eg.out_bf16 = h_;
     const int ig = tbegin(cGU + (M.prefill ? 0 : kDecOff));
+    if (ig >= 0 && !M.prefill) timed_[ig].sub = kGemmBucket + bucket_of(T);
     gemm(xa_, w.tgu, T, 2 * F_, d_, eg, dec);
     tend(ig, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
     EpiParams ed{};
@@ -638,6 +648,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ed.out_f32 = x_;
     ed.ldo = d_;
     const int idn = tbegin(cDown + (M.prefill ? 0 : kDecOff));
+    if (idn >= 0 && !M.prefill) timed_[idn].sub = kGemmBucket + bucket_of(T);
     const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
@@ -865,11 +876,14 @@ td_status CudaEngine::end_run(td_run_stats* st) {
   for (auto& tl : timed_) {
     float t = 0.f;
     cudaEventElapsedTime(&t, tl.a, tl.b);
-    KernelTiming& kt = timing_acc_[cls_names_[tl.cls]];
-    kt.launches++;
-    kt.ms += t;
-    kt.bytes += tl.bytes;
-    kt.flops += tl.flops;
+    for (int c : {tl.cls, tl.sub}) {
+      if (c < 0) continue;
+      KernelTiming& kt = timing_acc_[cls_names_[c]];
+      kt.launches++;
+      kt.ms += t;
+      kt.bytes += tl.bytes;
+      kt.flops += tl.flops;
+    }
     if (tl.cls == cStage) busy += t;
   }
   if (timing_ && ms > 0) {

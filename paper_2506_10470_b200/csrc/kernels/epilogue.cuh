@@ -146,4 +146,113 @@ TDP_DEV void epilogue_chunk(const EpiParams& ep, int T, int Nf, int f, int t0, c
   }
 }
 
+// Token-major tcgen05 epilogue (prefill GEMM): this thread owns token t and
+// holds features f0 .. f0+31 in v[] (consecutive TMEM columns), so RoPE pairs
+// (2i, 2i+1) and gate/up pairs are adjacent registers and every global access
+// is a 16-byte vector.  pos / slot are this token's position and KV slot.
+TDP_DEV void store_bf16x16(bf16* dst, const float* v) {
+  uint4 a, b;
+  a.x = pack_bf16x2(v[0], v[1]);
+  a.y = pack_bf16x2(v[2], v[3]);
+  a.z = pack_bf16x2(v[4], v[5]);
+  a.w = pack_bf16x2(v[6], v[7]);
+  b.x = pack_bf16x2(v[8], v[9]);
+  b.y = pack_bf16x2(v[10], v[11]);
+  b.z = pack_bf16x2(v[12], v[13]);
+  b.w = pack_bf16x2(v[14], v[15]);
+  reinterpret_cast<uint4*>(dst)[0] = a;
+  reinterpret_cast<uint4*>(dst)[1] = b;
+}
+
+TDP_DEV void epilogue_row(const EpiParams& ep, int Nf, int t, int f0, float* v, int pos, int slot) {
+  const bool full = f0 + 32 <= Nf;
+  switch (ep.mode) {
+    case kEpiF32: {
+      float* o = ep.out_f32 + (int64_t)t * ep.ldo + f0;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (f0 + j < Nf) o[j] = v[j];
+      }
+      break;
+    }
+    case kEpiResid: {
+      float* o = ep.out_f32 + (int64_t)t * ep.ldo + f0;
+      if (full) {
+        float4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = reinterpret_cast<const float4*>(o)[j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          reinterpret_cast<float4*>(o)[j] =
+              make_float4(x[j].x + v[4 * j], x[j].y + v[4 * j + 1], x[j].z + v[4 * j + 2], x[j].w + v[4 * j + 3]);
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (f0 + j < Nf) o[j] += v[j];
+      }
+      break;
+    }
+    case kEpiSwiGLU: {
+      float h[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) h[j] = silu(v[2 * j]) * v[2 * j + 1];
+      bf16* o = ep.out_bf16 + (int64_t)t * (Nf >> 1) + (f0 >> 1);
+      if (full) {
+        store_bf16x16(o, h);
+      } else {
+        for (int j = 0; j < 16; ++j)
+          if (f0 + 2 * j < Nf) o[j] = __float2bfloat16_rn(h[j]);
+      }
+      break;
+    }
+    case kEpiBF16: {
+      bf16* o = ep.out_bf16 + (int64_t)t * ep.ldo + f0;
+      if (full) {
+        store_bf16x16(o, v);
+        store_bf16x16(o + 16, v + 16);
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (f0 + j < Nf) o[j] = __float2bfloat16_rn(v[j]);
+      }
+      break;
+    }
+    case kEpiQKV: {
+      const int hd = ep.hd, half = hd >> 1;
+      const int qcols = ep.H * hd, kcols = ep.Hkv * hd;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {           // 16-feature groups (a group never spans two heads)
+        const int f = f0 + 16 * g;
+        if (f >= Nf) break;
+        float* w = v + 16 * g;
+        if (f < qcols + kcols) {              // rotate-half pairs (2i, 2i+1) at absolute position pos
+          const int i0 = (f % hd) >> 1;
+          const float4* cs = reinterpret_cast<const float4*>(ep.rope_cs + ((int64_t)pos * half + i0) * 2);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const float4 c2 = cs[p];          // (cos, sin) of pairs 2p and 2p+1
+            const float e0 = w[4 * p], o0 = w[4 * p + 1], e1 = w[4 * p + 2], o1 = w[4 * p + 3];
+            w[4 * p] = e0 * c2.x - o0 * c2.y;
+            w[4 * p + 1] = o0 * c2.x + e0 * c2.y;
+            w[4 * p + 2] = e1 * c2.z - o1 * c2.w;
+            w[4 * p + 3] = o1 * c2.z + e1 * c2.w;
+          }
+        }
+        bf16* dst;
+        if (f < qcols) {
+          dst = ep.out_bf16 + (int64_t)t * qcols + f;
+        } else {
+          const bool isk = f < qcols + kcols;
+          const int kn = f - (isk ? qcols : qcols + kcols);
+          dst = ep.kcache + ((((int64_t)(slot >> 4) * 2 + (isk ? 0 : 1)) * ep.Hkv + kn / hd) * kBlock + (slot & 15)) * hd +
+                kn % hd;
+        }
+        store_bf16x16(dst, w);
+      }
+      break;
+    }
+  }
+}
+
 }  // namespace tdp

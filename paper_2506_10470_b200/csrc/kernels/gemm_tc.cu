@@ -270,6 +270,134 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   }
 }
 
+// ----------------------------------------------------------------------------
+// Token-major tcgen05 GEMM for prefill micro-batches:
+//   MMA M = 128 tokens (A = activation tile via TMA, 128B swizzle), N = 256
+//   output features (B = two tile-packed 16 KB weight tiles via bulk copies),
+//   K = 64 per stage.  TMEM lane = token, column = feature, so the epilogue
+//   thread of a token holds 32 consecutive features per tcgen05.ld and writes
+//   16-byte vectors (epilogue_row).  Grid: x = token tile (fastest: the token
+//   tiles of one weight tile run together and share it through L2), y = 256-
+//   feature tile.
+template <int STAGES>
+__global__ void __launch_bounds__(192, 1)
+gemm_tn_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int kb_total,
+               EpiParams ep) {
+  constexpr int BNF = 256;
+  constexpr int X_BYTES = 128 * BK * 2;          // 16 KB
+  constexpr int W_BYTES = BNF * BK * 2;          // 32 KB
+  constexpr int STAGE_BYTES = X_BYTES + W_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accf = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 128;              // tokens
+  const int n0 = blockIdx.y * BNF;              // features
+  const int wt0 = n0 >> 7;                      // first 128-row packed weight tile
+  const int n_wt = min(2, ((Nf + 127) >> 7) - wt0);   // 1 if the last tile is a half tile
+  const uint32_t stage_tx = X_BYTES + n_wt * (W_BYTES / 2);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(BNF)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      auto load_w = [&](uint8_t* dst, int kb, uint64_t* bar) {
+        for (int h = 0; h < n_wt; ++h)
+          bulk_load(dst + h * (W_BYTES / 2), wpk + (((int64_t)(wt0 + h) * kb_total + kb) << 13), W_BYTES / 2, bar, pol);
+      };
+      const int pre = min(kb_total, STAGES);
+      for (int i = 0; i < pre; ++i) {            // weights first (independent of the previous kernel)
+        mbar_expect_tx(&full[i], stage_tx);
+        load_w(smem + i * STAGE_BYTES + X_BYTES, i, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_2d(smem + i * STAGE_BYTES, &tmX, i * BK, m0, &full[i]);
+      for (int i = pre; i < kb_total; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], stage_tx);
+        load_w(sa + X_BYTES, i, &full[s]);
+        tma_load_2d(sa, &tmX, i * BK, m0, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BNF >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      for (int i = 0; i < kb_total; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        const uint64_t ad = smem_desc_sw128(sa);
+        const uint64_t bd = smem_desc_sw128(sa + X_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_f16(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(accf);
+    }
+  } else {
+    pdl_wait();
+    mbar_wait(accf, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int t = m0 + q * 32 + lane;           // this thread's token
+    const bool tok = t < T;
+    int pos = 0, slot = 0;
+    if (tok && ep.mode == kEpiQKV) {
+      pos = ep.pos[t];
+      slot = ep.slot[t];
+    }
+#pragma unroll 1
+    for (int c = 0; c < BNF; c += 32) {
+      if (n0 + c >= Nf) break;
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (tok) epilogue_row(ep, Nf, t, n0 + c, v, pos, slot);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BNF) : "memory");
+  }
+}
+
 // split-K reduction: sums the partials in split order (deterministic) and
 // applies the fused epilogue; grid-stride over (token, feature pair)
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
@@ -389,9 +517,31 @@ int effective_splits(int K, int splits) {
   return (kb_total + kps - 1) / kps;
 }
 
+static bool tn_enabled() {   // TDPIPE_TN=0: prefill through the swap-AB kernel (A/B measurements)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TDPIPE_TN");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
                    int* counters, bool decode, cudaStream_t st, bool defer_reduce) {
   if (T <= 0) return 1;
+  if (!decode && W.packed && tn_enabled() && T > 128) {
+    // prefill: token-major tiles (vectorised epilogue)
+    constexpr int STAGES = 4;
+    constexpr int sm = STAGES * (128 * BK * 2 + 256 * BK * 2) + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_tn_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      attr = true;
+    }
+    dim3 grid((T + 127) / 128, (W.rows + 255) / 256, 1);
+    launch_k(gemm_tn_kernel<STAGES>, grid, dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T, W.K / BK, ep);
+    return 1;
+  }
   switch (tc_bn_for(T, decode)) {
     // <= 110 KB of smem for BN <= 128 so that two CTAs share an SM
     case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, defer_reduce, st); break;
