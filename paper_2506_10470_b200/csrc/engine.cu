@@ -153,6 +153,7 @@ class CudaEngine : public Engine {
   float* ws_ = nullptr;
   int64_t ws_cap_ = 0;
   int* counters_ = nullptr;
+  int* attn_cnt_ = nullptr;   // decode-attention split tickets [capN * Hkv]
   // work
   int64_t capT_ = 0, capN_ = 0, capBlk_ = 0;
   float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
@@ -376,6 +377,7 @@ void CudaEngine::release() {
   cudaFree(arena_);
   cudaFree(ws_);
   cudaFree(counters_);
+  cudaFree(attn_cnt_);
   for (int i = 0; i < kRing; ++i) {
     if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
     cudaFree(dmeta_[i]);
@@ -415,6 +417,9 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&logits_, n * V_ * 4));
   max_splits_cap_ = (int)cdiv(s_.max_seq_len, 128);
   CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
+  cudaFree(attn_cnt_);
+  CK(cudaMalloc(&attn_cnt_, n * Hkv_ * sizeof(int)));
+  CK(cudaMemsetAsync(attn_cnt_, 0, n * Hkv_ * sizeof(int), st_));
   // metadata ring: per seq 5 ints + bt, per token 4 ints, header
   const int64_t need = 16 + 5 * n + 2 + n * maxblk + 4 * T + 64;
   if (need > meta_cap_) {
@@ -618,12 +623,13 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       int split = 512;
       while (split > 128 && (int64_t)n * Hkv_ * cdiv(M.max_ctx, split) < 4 * 148) split >>= 1;
       const int ms = (int)cdiv(M.max_ctx, split);
-      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split};
+      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split,
+                          attn_cnt_};
       const int ida = tbegin(cDecAttn);
       if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
       launch_decode_attn(dp, st_);
       tend(ida, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
-      launches_ += ms > 1 ? 2 : 1;
+      launches_++;
     }
     EpiParams eo{};
     eo.mode = kEpiResid;

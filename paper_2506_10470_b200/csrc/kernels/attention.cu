@@ -65,19 +65,27 @@ decode_attn_kernel(DecodeAttnParams p) {
   }
   const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
   const int64_t head_stride = (int64_t)kBlock * HD;           // one (blk, kv, head) page
-  for (int base = t_begin; base < t_end; base += NW * TPW * U) {
-    uint4 kr[U], vr[U];
-    bool valid[U];
+  constexpr int STEP = NW * TPW * U;
+  // software pipeline (G <= 2): the next step's K/V loads are in flight while
+  // this step's softmax runs (two steps of 16-byte loads per thread)
+  constexpr bool PF = G <= 2;
+  uint4 kr[U], vr[U], kn[U], vn[U];
+  bool valid[U], vnx[U];
+  auto issue = [&](int base, uint4* K, uint4* Vv, bool* ok) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int t = base + (u * NW + warp) * TPW + tg;
-      valid[u] = t < t_end;
-      const int tt = valid[u] ? t : t_begin;
+      ok[u] = t < t_end;
+      const int tt = ok[u] ? t : t_begin;
       const int blk = bt[tt >> 4];
-      const int64_t kbase = (((int64_t)blk * 2) * p.Hkv + kh) * head_stride + (tt & 15) * HD + sub * 8;
-      kr[u] = ld_nc_v4(p.kv + kbase);
-      vr[u] = ld_nc_v4(p.kv + kbase + (int64_t)p.Hkv * head_stride);
+      const int64_t kb = (((int64_t)blk * 2) * p.Hkv + kh) * head_stride + (tt & 15) * HD + sub * 8;
+      K[u] = ld_nc_v4(p.kv + kb);
+      Vv[u] = ld_nc_v4(p.kv + kb + (int64_t)p.Hkv * head_stride);
     }
+  };
+  issue(t_begin, kr, vr, valid);
+  for (int base = t_begin; base < t_end; base += STEP) {
+    if (PF && base + STEP < t_end) issue(base + STEP, kn, vn, vnx);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float kf[8], vf[8];
@@ -99,6 +107,18 @@ decode_attn_kernel(DecodeAttnParams p) {
           for (int i = 0; i < 8; ++i) acc[g][i] = fmaf(pr, vf[i], acc[g][i] * corr);
           m[g] = mn;
         }
+      }
+    }
+    if (base + STEP < t_end) {
+      if (PF) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          kr[u] = kn[u];
+          vr[u] = vn[u];
+          valid[u] = vnx[u];
+        }
+      } else {
+        issue(base + STEP, kr, vr, valid);
       }
     }
   }
@@ -149,32 +169,39 @@ decode_attn_kernel(DecodeAttnParams p) {
       p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
     } else {
       float* part = p.part + (((int64_t)seq * H + h) * p.max_splits + split) * (HD + 2);
-      part[2 + dim] = A;
-      if (dim == 0) { part[0] = M; part[1] = L; }
+      __stcg(part + 2 + dim, A);
+      if (dim == 0) {
+        __stcg(part, M);
+        __stcg(part + 1, L);
+      }
     }
   }
-}
-
-__global__ void decode_combine_kernel(DecodeAttnParams p, int hd) {
-  pdl_trigger();
-  pdl_wait();
-  const int seq = blockIdx.y, h = blockIdx.x;
-  const int ctx = p.ctx[seq];
-  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
-  if (n_splits <= 1) return;
-  const float* part = p.part + ((int64_t)seq * p.H + h) * p.max_splits * (hd + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < n_splits; ++s) M = fmaxf(M, part[s * (hd + 2)]);
-  for (int dim = threadIdx.x; dim < hd; dim += blockDim.x) {
+  if (n_splits == 1) return;
+  // the last split CTA of this (sequence, kv head) merges all splits in split
+  // order (deterministic) -- no separate combine launch
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[seq * p.Hkv + kh], 1) == n_splits - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
+    const int g = e / HD, dim = e % HD;
+    const int h = kh * G + g;
+    const float* part = p.part + ((int64_t)seq * H + h) * p.max_splits * (HD + 2);
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < n_splits; ++s2) M = fmaxf(M, __ldcg(part + s2 * (HD + 2)));
     float L = 0.f, A = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float* ps = part + s * (hd + 2);
-      const float c = exp2f(ps[0] - M);
-      L += ps[1] * c;
-      A += ps[2 + dim] * c;
+    for (int s2 = 0; s2 < n_splits; ++s2) {
+      const float* ps = part + s2 * (HD + 2);
+      const float c = exp2f(__ldcg(ps) - M);
+      L += __ldcg(ps + 1) * c;
+      A += __ldcg(ps + 2 + dim) * c;
     }
-    p.o[((int64_t)seq * p.H + h) * hd + dim] = __float2bfloat16_rn(A / L);
+    p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
   }
+  if (threadIdx.x == 0) p.counters[seq * p.Hkv + kh] = 0;
 }
 
 template <int HD>
@@ -188,7 +215,7 @@ static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
     case 8: launch_k(decode_attn_kernel<HD, 8>, grid, dim3(128), 0, st, p); break;
     default: return;
   }
-  if (p.max_splits > 1) launch_k(decode_combine_kernel, dim3(p.H, p.n), dim3(128), 0, st, p, HD);
+
 }
 
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {

@@ -80,6 +80,7 @@ struct DecodeAttnParams {
   int max_splits;
   int n, H, Hkv, hd;
   int split_tokens;      // context tokens per split (multiple of 16)
+  int* counters;         // [n * Hkv] zero-initialised split tickets (reset by the merging CTA)
 };
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 
