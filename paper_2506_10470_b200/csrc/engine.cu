@@ -415,7 +415,7 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&ob_, T * H_ * hd_ * 2));
   CK(cudaMalloc(&h_, T * F_ * 2));
   CK(cudaMalloc(&logits_, n * V_ * 4));
-  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 128);
+  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 64);
   CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
   cudaFree(attn_cnt_);
   CK(cudaMalloc(&attn_cnt_, n * Hkv_ * sizeof(int)));
@@ -474,6 +474,9 @@ td_status CudaEngine::make_x_ops() {
 int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
                      bool defer) {
   int splits = 1;
+  // 129..256-token decode batches of the wide GEMMs (QKV, gate/up, LM head) are
+  // closer to the tensor roof than to HBM: take the token-major kernel
+  if (decode && T > 128 && N >= 8192) decode = false;
   if (decode) {
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
@@ -619,9 +622,12 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       tend(ip, 0, 0);
       launches_++;
     } else {
-      // split size: 512 tokens unless the grid would not fill the GPU (>= 4 CTAs per SM)
-      int split = 512;
-      while (split > 128 && (int64_t)n * Hkv_ * cdiv(M.max_ctx, split) < 4 * 148) split >>= 1;
+      // splits per sequence: fill one wave of resident CTAs (4 per SM at the
+      // kernel's register budget) without spilling into a second wave; >= 64
+      // context tokens per split
+      const int64_t base = (int64_t)n * Hkv_;
+      int ns = (int)std::max<int64_t>(1, std::min<int64_t>((4 * 148) / base, cdiv(M.max_ctx, 64)));
+      const int split = (int)cdiv(cdiv(M.max_ctx, ns), 16) * 16;
       const int ms = (int)cdiv(M.max_ctx, split);
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split,
                           attn_cnt_};
