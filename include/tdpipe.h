@@ -194,6 +194,15 @@ td_status td_load_profile(struct td_ctx* ctx, const char* csv);
  * Copies min(cap, need) bytes; *need = full length (without NUL). */
 td_status td_get_log(struct td_ctx* ctx, char* buf, size_t cap, size_t* need);
 
+/* Timed replay of the whole schedule on an S-stage pipeline model (no GPU
+ * work): every micro-batch occupies each stage for the frozen profile time
+ * (Tpre[tokens] or Tdec[batch], per-stage), stages are FIFO servers, a return
+ * reaches the controller host_return_ns after the last stage.  Produces the
+ * same decision log as td_run and fills makespan / tokens/s / bubble /
+ * busy_ns -- used to project multi-GPU TD-Pipe vs PP+SB from measured
+ * per-stage B200 times.  Needs a loaded profile table. */
+td_status td_simulate(struct td_ctx* ctx, td_run_stats* st, int64_t host_return_ns);
+
 /* Model / pool facts: kv_blocks, layers of `stage`, weight bytes per stage. */
 td_status td_info(struct td_ctx* ctx, int64_t* kv_blocks, int32_t* n_stages,
                   int64_t* weight_bytes_stage0, int64_t* kv_bytes_per_block);

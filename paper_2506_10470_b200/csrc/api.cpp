@@ -239,6 +239,101 @@ extern "C" td_status td_run(td_ctx* c, td_run_stats* st) {
   return TD_OK;
 }
 
+// Timed pipeline model for td_simulate: stages are FIFO servers with the
+// frozen per-stage profile times; launch time = the controller event time.
+struct SimHooks : ExecHooks {
+  int S;
+  const std::vector<int64_t>& tdec;
+  const std::vector<int64_t>& tpre;
+  int64_t host_ns;
+  std::vector<int64_t> free_at, busy;
+  std::vector<int64_t> ret;   // by micro-batch id
+  int64_t now = 0, makespan = 0;
+  SimHooks(int s, const std::vector<int64_t>& d, const std::vector<int64_t>& p, int64_t h)
+      : S(s), tdec(d), tpre(p), host_ns(h), free_at(s, 0), busy(s, 0) {}
+  static int64_t at(const std::vector<int64_t>& t, int64_t i) {
+    return t[std::min<int64_t>(std::max<int64_t>(i, 1), (int64_t)t.size() - 1)];
+  }
+  int launch(const MicroBatch& mb, const std::vector<Req>&) override {
+    int64_t tok = 0;
+    for (int q : mb.q_len) tok += q;
+    const int64_t t = mb.kind == 'P' ? at(tpre, tok) : at(tdec, (int64_t)mb.members.size());
+    int64_t arrive = now;
+    for (int s = 0; s < S; ++s) {
+      const int64_t start = std::max(arrive, free_at[s]);
+      free_at[s] = start + t;
+      busy[s] += t;
+      arrive = start + t;
+    }
+    if ((int64_t)ret.size() <= mb.mid) ret.resize(mb.mid + 1, 0);
+    ret[mb.mid] = arrive + host_ns;
+    return 0;
+  }
+  int returned(const MicroBatch& mb) override {
+    now = std::max(now, ret[mb.mid]);
+    makespan = std::max(makespan, now);
+    return 0;
+  }
+};
+
+extern "C" td_status td_simulate(td_ctx* c, td_run_stats* st, int64_t host_return_ns) {
+  if (!c || !st) return TD_EINVAL;
+  if (c->tdec.size() < 2 || c->tpre.size() < 2) return fail(c, TD_ESTATE, "td_simulate needs a profile table");
+  SchedOptions so;
+  so.W = c->n_stages;
+  so.B = c->opt.block_size;
+  so.C = c->kv_blocks;
+  so.budget = c->opt.prefill_token_budget;
+  so.max_seqs = c->opt.max_batch_seqs;
+  so.fp_stride = c->opt.fp_stride;
+  so.fp_horizon = c->opt.fp_horizon;
+  so.policy = c->opt.policy;
+  so.steal = c->opt.steal;
+  so.check_before_launch = c->opt.alg1_check_before_launch;
+  so.eq2_bubble_scale = c->opt.eq2_bubble_scale;
+  so.p2d_kv_permille = c->opt.p2d_kv_permille;
+  so.d2p_finish_permille = c->opt.d2p_finish_permille;
+  std::vector<Req> reqs(c->reqs.size());
+  for (size_t i = 0; i < c->reqs.size(); ++i) {
+    reqs[i].rid = (int)i;
+    reqs[i].n_prompt = (int)c->reqs[i].prompt.size();
+    reqs[i].L = reqs[i].n_prompt;
+    reqs[i].P = c->reqs[i].predicted;
+    reqs[i].N = c->reqs[i].max_new;
+  }
+  Controller ctl(so, reqs, c->tdec, c->tpre, c->opt.log_decisions != 0);
+  SimHooks sim(c->n_stages, c->tdec, c->tpre, host_return_ns);
+  if (int rc = ctl.run(&sim)) return fail(c, rc < 0 ? rc : TD_ESTATE, ctl.error);
+  td_run_stats s{};
+  const auto& ss = ctl.stats();
+  int64_t gen = 0;
+  for (const auto& r : ctl.reqs()) gen += r.n_out;
+  s.n_requests = (int64_t)reqs.size();
+  s.prompt_tokens = ss.prompt_tokens;
+  s.generated_tokens = gen;
+  s.makespan_ns = sim.makespan;
+  s.n_microbatches = ss.n_mb;
+  s.n_prefill_mb = ss.n_prefill;
+  s.n_decode_mb = ss.n_decode;
+  s.n_p2d = ss.p2d;
+  s.n_d2p = ss.d2p;
+  s.n_stolen = ss.stolen;
+  s.n_evicted = ss.evicted;
+  double busy = 0;
+  for (int i = 0; i < c->n_stages; ++i) {
+    busy += (double)sim.busy[i];
+    if (i < 8) s.busy_ns[i] = sim.busy[i];
+  }
+  if (sim.makespan > 0) {
+    s.gen_tokens_per_s = gen * 1e9 / (double)sim.makespan;
+    s.total_tokens_per_s = (gen + ss.prompt_tokens) * 1e9 / (double)sim.makespan;
+    s.bubble_frac = 1.0 - busy / ((double)c->n_stages * (double)sim.makespan);
+  }
+  c->log = ctl.log();
+  *st = s;
+  return TD_OK;
+}
+
 static td_status cache_outputs(td_ctx* c) {
   if (c->outputs_cached) return TD_OK;
   if (!c->have_run) return fail(c, TD_ESTATE, "td_run has not completed");
