@@ -203,6 +203,12 @@ td_status td_get_log(struct td_ctx* ctx, char* buf, size_t cap, size_t* need);
  * per-stage B200 times.  Needs a loaded profile table. */
 td_status td_simulate(struct td_ctx* ctx, td_run_stats* st, int64_t host_return_ns);
 
+/* Write the last td_simulate run as a Chrome trace (chrome://tracing /
+ * Perfetto JSON): one complete event per (micro-batch, stage) on thread =
+ * stage, plus a "kv_used_blocks" counter track sampled at every launch
+ * (the KV-usage timeline of PAPER.md:580-585 fig:memory_usage). */
+td_status td_write_trace(struct td_ctx* ctx, const char* path);
+
 /* Model / pool facts: kv_blocks, layers of `stage`, weight bytes per stage. */
 td_status td_info(struct td_ctx* ctx, int64_t* kv_blocks, int32_t* n_stages,
                   int64_t* weight_bytes_stage0, int64_t* kv_bytes_per_block);

@@ -34,6 +34,10 @@ struct td_ctx {
   std::unique_ptr<Engine> engine;
   std::vector<std::vector<int32_t>> outputs;   // cached after first td_get_output
   bool outputs_cached = false;
+  // last td_simulate: (mid, kind, stage, start_ns, end_ns) and (t_ns, used blocks)
+  struct Span { int64_t mid; char kind; int stage; int64_t a, b; };
+  std::vector<Span> spans;
+  std::vector<std::pair<int64_t, int64_t>> kv_samples;
 };
 
 static td_status fail(td_ctx* c, td_status st, const std::string& m) {
@@ -249,12 +253,14 @@ struct SimHooks : ExecHooks {
   std::vector<int64_t> free_at, busy;
   std::vector<int64_t> ret;   // by micro-batch id
   int64_t now = 0, makespan = 0;
+  std::vector<td_ctx::Span>* spans = nullptr;
+  std::vector<std::pair<int64_t, int64_t>>* kv = nullptr;
   SimHooks(int s, const std::vector<int64_t>& d, const std::vector<int64_t>& p, int64_t h)
       : S(s), tdec(d), tpre(p), host_ns(h), free_at(s, 0), busy(s, 0) {}
   static int64_t at(const std::vector<int64_t>& t, int64_t i) {
     return t[std::min<int64_t>(std::max<int64_t>(i, 1), (int64_t)t.size() - 1)];
   }
-  int launch(const MicroBatch& mb, const std::vector<Req>&) override {
+  int launch(const MicroBatch& mb, const std::vector<Req>& reqs) override {
     int64_t tok = 0;
     for (int q : mb.q_len) tok += q;
     const int64_t t = mb.kind == 'P' ? at(tpre, tok) : at(tdec, (int64_t)mb.members.size());
@@ -264,6 +270,12 @@ struct SimHooks : ExecHooks {
       free_at[s] = start + t;
       busy[s] += t;
       arrive = start + t;
+      if (spans) spans->push_back({mb.mid, mb.kind, s, start, start + t});
+    }
+    if (kv) {
+      int64_t used = 0;
+      for (const auto& r : reqs) used += (int64_t)r.blocks.size();
+      kv->push_back({now, used});
     }
     if ((int64_t)ret.size() <= mb.mid) ret.resize(mb.mid + 1, 0);
     ret[mb.mid] = arrive + host_ns;
@@ -303,6 +315,10 @@ extern "C" td_status td_simulate(td_ctx* c, td_run_stats* st, int64_t host_retur
   }
   Controller ctl(so, reqs, c->tdec, c->tpre, c->opt.log_decisions != 0);
   SimHooks sim(c->n_stages, c->tdec, c->tpre, host_return_ns);
+  c->spans.clear();
+  c->kv_samples.clear();
+  sim.spans = &c->spans;
+  sim.kv = &c->kv_samples;
   if (int rc = ctl.run(&sim)) return fail(c, rc < 0 ? rc : TD_ESTATE, ctl.error);
   td_run_stats s{};
   const auto& ss = ctl.stats();
@@ -331,6 +347,29 @@ extern "C" td_status td_simulate(td_ctx* c, td_run_stats* st, int64_t host_retur
   }
   c->log = ctl.log();
   *st = s;
+  return TD_OK;
+}
+
+extern "C" td_status td_write_trace(td_ctx* c, const char* path) {
+  if (!c || !path) return TD_EINVAL;
+  std::ofstream f(path);
+  if (!f) return fail(c, TD_EINVAL, "cannot open trace path");
+  f << "{\"traceEvents\":[";
+  bool first = true;
+  char buf[256];
+  for (const auto& sp : c->spans) {
+    snprintf(buf, sizeof buf, "%s{\"name\":\"%c %lld\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":0,\"tid\":%d}",
+             first ? "" : ",", sp.kind, (long long)sp.mid, sp.a / 1e3, (sp.b - sp.a) / 1e3, sp.stage);
+    f << buf;
+    first = false;
+  }
+  for (const auto& kv : c->kv_samples) {
+    snprintf(buf, sizeof buf, "%s{\"name\":\"kv_used_blocks\",\"ph\":\"C\",\"ts\":%.3f,\"pid\":0,\"args\":{\"blocks\":%lld}}",
+             first ? "" : ",", kv.first / 1e3, (long long)kv.second);
+    f << buf;
+    first = false;
+  }
+  f << "]}\n";
   return TD_OK;
 }
 

@@ -63,7 +63,7 @@ class td_batch(C.Structure):
 EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td_submit", "td_upload",
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
-           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_simulate"]
+           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_simulate", "td_write_trace"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_nccl_ids.argtypes = [C.c_void_p]
     lib.td_bench_gemm.argtypes = [C.c_int32] * 8 + [P(C.c_float)]
     lib.td_simulate.argtypes = [C.c_void_p, P(td_run_stats), C.c_int64]
+    lib.td_write_trace.argtypes = [C.c_void_p, C.c_char_p]
     lib.td_test_gemm.argtypes = [C.c_int32, P(C.c_uint16), P(C.c_uint16), C.c_int32, C.c_int32, C.c_int32,
                                  C.c_int32, C.c_int32, P(C.c_float)]
     for f in EXPORTS:
@@ -195,6 +196,9 @@ class TDPipe:
         st = td_run_stats()
         self._check(lib().td_simulate(self.ctx, C.byref(st), int(host_return_ns)), "td_simulate")
         return st.as_dict()
+
+    def td_write_trace(self, path: str):
+        self._check(lib().td_write_trace(self.ctx, path.encode()), "td_write_trace")
 
     def td_get_output(self, rid: int) -> np.ndarray:
         n = C.c_int32(0)

@@ -28,3 +28,30 @@ def test_simulate_matches_run_and_bounds(tmp_path):
             assert st["generated_tokens"] == sum(r.max_new_tokens for r in wl.requests)
             if S == 1:
                 assert st["bubble_frac"] < 0.05                   # one stage: only host-return gaps
+
+
+def test_trace_export(tmp_path):
+    """The Chrome trace holds one span per (micro-batch, stage), spans on a stage
+    never overlap, and the bubble recomputed from the trace equals td_simulate's."""
+    import json
+    csv = str(tmp_path / "p.csv")
+    write_profile_csv(csv, *synthetic_profile(512, 2048, dec_base_ns=3_000_000, dec_per_req_ns=4_000, knee=96))
+    wl = generate_workload(120, 256, 9, in_max=400, out_max=300)
+    shape = dataclasses.replace(SHAPES["tiny"].with_layers(8), max_seq_len=4096)
+    t = TDPipe(shape, 4, executor=TD_EXEC_NULL, kv_blocks=1200, profile_csv=csv)
+    t.submit_workload(wl)
+    st = t.td_simulate(20_000)
+    path = str(tmp_path / "trace.json")
+    t.td_write_trace(path)
+    ev = json.load(open(path))["traceEvents"]
+    spans = [e for e in ev if e["ph"] == "X"]
+    kv = [e for e in ev if e["ph"] == "C"]
+    assert len(spans) == 4 * st["n_microbatches"] and len(kv) == st["n_microbatches"]
+    busy = 0.0
+    for s in range(4):
+        ss = sorted((e["ts"], e["ts"] + e["dur"]) for e in spans if e["tid"] == s)
+        assert all(a[1] <= b[0] + 1e-6 for a, b in zip(ss, ss[1:]))
+        busy += sum(b - a for a, b in ss)
+    bubble = 1 - busy / (4 * st["makespan_ns"] / 1e3)
+    assert abs(bubble - st["bubble_frac"]) < 1e-3
+    assert max(e["args"]["blocks"] for e in kv) <= 1200
