@@ -48,6 +48,9 @@ TDP_DEV void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   }
 }
+TDP_DEV void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 TDP_DEV void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
@@ -398,6 +401,151 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__
   }
 }
 
+// Persistent variant of gemm_tn_kernel: one CTA per SM walks the (token tile,
+// feature tile) grid (token tile fastest, so concurrently running CTAs share a
+// weight tile through L2); the two 256-column TMEM accumulators are double
+// buffered so the epilogue of tile i overlaps the MMAs of tile i+1, and the
+// smem ring runs continuously across tiles.
+template <int STAGES>
+__global__ void __launch_bounds__(192, 1)
+gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int kb_total,
+                EpiParams ep) {
+  constexpr int BNF = 256;
+  constexpr int X_BYTES = 128 * BK * 2;
+  constexpr int W_BYTES = BNF * BK * 2;
+  constexpr int STAGE_BYTES = X_BYTES + W_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;      // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MT = (T + 127) / 128;
+  const int NT = (Nf + BNF - 1) / BNF;
+  const int n_tiles = MT * NT;
+  const int wtiles = (Nf + 127) >> 7;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(2 * BNF)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int it = 0;   // global k-block counter (ring position)
+      bool waited = false;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int m0 = (tile % MT) * 128, nt = tile / MT;
+        const int wt0 = nt * 2;
+        const int n_wt = min(2, wtiles - wt0);
+        const uint32_t stage_tx = X_BYTES + n_wt * (W_BYTES / 2);
+        for (int kb = 0; kb < kb_total; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+          if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], stage_tx);
+          for (int h = 0; h < n_wt; ++h)
+            bulk_load(sa + X_BYTES + h * (W_BYTES / 2), wpk + (((int64_t)(wt0 + h) * kb_total + kb) << 13),
+                      W_BYTES / 2, &full[s], pol);
+          if (!waited) {   // activations come from the previous kernel (PDL)
+            pdl_wait();
+            waited = true;
+          }
+          tma_load_2d(sa, &tmX, kb * BK, m0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BNF >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      int it = 0, i = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+        const int a = i & 1;
+        const uint32_t aph = (uint32_t)(i >> 1) & 1u;
+        if (i >= 2) mbar_wait(&tempty[a], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(a * BNF);
+        for (int kb = 0; kb < kb_total; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          const uint64_t ad = smem_desc_sw128(sa);
+          const uint64_t bd = smem_desc_sw128(sa + X_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_f16(acc, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[a]);
+      }
+    }
+  } else {
+    pdl_wait();
+    const int q = warp & 3;
+    int i = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+      const int a = i & 1;
+      const int m0 = (tile % MT) * 128, n0 = (tile / MT) * BNF;
+      mbar_wait(&tfull[a], (uint32_t)(i >> 1) & 1u);
+      tc_fence_after();
+      const int t = m0 + q * 32 + lane;
+      const bool tok = t < T;
+      int pos = 0, slot = 0;
+      if (tok && ep.mode == kEpiQKV) {
+        pos = ep.pos[t];
+        slot = ep.slot[t];
+      }
+#pragma unroll 1
+      for (int c = 0; c < BNF; c += 32) {
+        if (n0 + c >= Nf) break;
+        uint32_t r[32];
+        tmem_ld32(tmem + (uint32_t)(a * BNF) + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (tok) epilogue_row(ep, Nf, t, n0 + c, v, pos, slot);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BNF) : "memory");
+  }
+}
+
 // split-K reduction: sums the partials in split order (deterministic) and
 // applies the fused epilogue; grid-stride over (token, feature pair)
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
@@ -517,6 +665,15 @@ int effective_splits(int K, int splits) {
   return (kb_total + kps - 1) / kps;
 }
 
+static bool tnp_enabled() {   // TDPIPE_TNP=0: non-persistent token-major kernel (A/B)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TDPIPE_TNP");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 static bool tn_enabled() {   // TDPIPE_TN=0: prefill through the swap-AB kernel (A/B measurements)
   static int on = -1;
   if (on < 0) {
@@ -537,6 +694,17 @@ int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const Epi
     if (!attr) {
       cudaFuncSetAttribute(gemm_tn_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       attr = true;
+    }
+    if (tnp_enabled()) {
+      static bool attr2 = false;
+      if (!attr2) {
+        cudaFuncSetAttribute(gemm_tnp_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        attr2 = true;
+      }
+      const int tiles = ((T + 127) / 128) * ((W.rows + 255) / 256);
+      launch_k(gemm_tnp_kernel<STAGES>, dim3(std::min(tiles, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows,
+               T, W.K / BK, ep);
+      return 1;
     }
     dim3 grid((T + 127) / 128, (W.rows + 255) / 256, 1);
     launch_k(gemm_tn_kernel<STAGES>, grid, dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T, W.K / BK, ep);
