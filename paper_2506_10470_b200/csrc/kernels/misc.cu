@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x
 void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* rows, int n, int d, float eps,
                     cudaStream_t st) {
   if (n <= 0) return;
-  launch_k(rmsnorm_kernel<256>, dim3(n), dim3(256), 0, st, x, g, out, rows, d, eps);
+  if (n < 148 && d >= 4096)
+    launch_k(rmsnorm_kernel<1024>, dim3(n), dim3(1024), 0, st, x, g, out, rows, d, eps);
+  else
+    launch_k(rmsnorm_kernel<256>, dim3(n), dim3(256), 0, st, x, g, out, rows, d, eps);
 }
 
 // ---------------------------------------------- split-K reduce + resid + norm
@@ -199,7 +202,12 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict_
 void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
                        cudaStream_t st) {
   if (T <= 0) return;
-  launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps);
+  // few rows (small decode batches): one wide CTA per row so a row's partial
+  // loads are all in flight at once
+  if (T < 148 && d >= 4096)
+    launch_k(resid_norm_kernel<1024>, dim3(T), dim3(1024), 0, st, ws, splits, x, g, out, T, d, eps);
+  else
+    launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps);
 }
 
 // -------------------------------------------------------------------- argmax
