@@ -171,7 +171,8 @@ def run_ours(args):
     L = np.array([len(r.prompt) for r in wl.requests])
     P = np.array([r.predicted_len for r in wl.requests])
     ctx_rep = int(L.sum() // n_req + (P.sum() // n_req) // 2)
-    prof = os.path.join(tempfile.gettempdir(), f"tdpipe_profile_{os.getpid()}.csv")
+    prof = os.path.join("gpurun_out" if os.path.isdir("gpurun_out") else tempfile.gettempdir(),
+                        f"tdpipe_profile_{args.config}_{os.getpid()}.csv")
     t0 = time.perf_counter()
     t.td_profile(prof, min(1024, max(n_req, 1)), 2048, ctx_rep)
     prof_s = time.perf_counter() - t0
