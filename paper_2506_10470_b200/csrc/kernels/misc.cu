@@ -8,8 +8,12 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace tdp {
 
@@ -199,15 +203,86 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict_
   }
 }
 
+// Small decode batches: a row is split over a cluster of RC CTAs (RC*128
+// threads); each reduces its slice of the split-K partials, and the row's sum
+// of squares is all-reduced through distributed shared memory, so the whole
+// GPU -- not T SMs -- streams the partials.
+template <int RC>
+__global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __restrict__ ws, int splits,
+                                                                  float* __restrict__ x, const bf16* __restrict__ g,
+                                                                  bf16* __restrict__ out, int T, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  const int t = blockIdx.y;
+  const int rank = (int)cl.block_rank();
+  const int per = d / RC;                      // elements of this CTA's slice
+  const int j0 = rank * per / 4;               // float4 index
+  float4* xr = reinterpret_cast<float4*>(x + (int64_t)t * d);
+  __shared__ float red[4];
+  __shared__ float part_ss;
+  float ss = 0.f;
+  for (int j = j0 + threadIdx.x; j < j0 + per / 4; j += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float4 p = __ldcg(reinterpret_cast<const float4*>(ws + ((int64_t)s * T + t) * d) + j);
+      acc.x += p.x;
+      acc.y += p.y;
+      acc.z += p.z;
+      acc.w += p.w;
+    }
+    float4 v = xr[j];
+    v.x += acc.x;
+    v.y += acc.y;
+    v.z += acc.z;
+    v.w += acc.w;
+    xr[j] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) part_ss = red[0] + red[1] + red[2] + red[3];
+  cl.sync();
+  if (!g) return;
+  float tot = 0.f;
+  for (int r = 0; r < RC; ++r) tot += *cl.map_shared_rank(&part_ss, r);   // fixed order: deterministic
+  cl.sync();                                   // peers keep their smem until everyone has read it
+  const float inv = rsqrtf(tot / (float)d + eps);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g);
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)t * d);
+  for (int j = j0 + threadIdx.x; j < j0 + per / 4; j += 128) {
+    const float4 v = xr[j];
+    const float2 ga = __bfloat1622float2(g2[2 * j]);
+    const float2 gb = __bfloat1622float2(g2[2 * j + 1]);
+    uint2 pk;
+    pk.x = pack_bf16x2(v.x * inv * ga.x, v.y * inv * ga.y);
+    pk.y = pack_bf16x2(v.z * inv * gb.x, v.w * inv * gb.y);
+    o[j] = pk;
+  }
+}
+
 void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
                        cudaStream_t st) {
   if (T <= 0) return;
-  // few rows (small decode batches): one wide CTA per row so a row's partial
-  // loads are all in flight at once
-  if (T < 148 && d >= 4096)
-    launch_k(resid_norm_kernel<1024>, dim3(T), dim3(1024), 0, st, ws, splits, x, g, out, T, d, eps);
-  else
+  if (T <= 64 && d % (8 * 4) == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(8, T);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 8;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<8>, ws, splits, x, g, out, T, d, eps);
+  } else {
     launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps);
+  }
 }
 
 // -------------------------------------------------------------------- argmax
