@@ -154,6 +154,7 @@ class CudaEngine : public Engine {
   int64_t ws_cap_ = 0;
   int* counters_ = nullptr;
   int* attn_cnt_ = nullptr;   // decode-attention split tickets [capN * Hkv]
+  std::vector<int> mb_ctx_;   // context length per sequence of the micro-batch being enqueued
   // work
   int64_t capT_ = 0, capN_ = 0, capBlk_ = 0;
   float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
@@ -415,7 +416,7 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&ob_, T * H_ * hd_ * 2));
   CK(cudaMalloc(&h_, T * F_ * 2));
   CK(cudaMalloc(&logits_, n * V_ * 4));
-  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 64);
+  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 128);
   CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
   cudaFree(attn_cnt_);
   CK(cudaMalloc(&attn_cnt_, n * Hkv_ * sizeof(int)));
@@ -526,8 +527,10 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
   M.total = off;
   int32_t* h = hmeta_[r];
   int t = 0;
+  mb_ctx_.resize(n);
   for (int i = 0; i < n; ++i) {
     const int ctx = q_start[i] + q_len[i];
+    mb_ctx_[i] = ctx;
     h[M.o_ctx + i] = ctx;
     const int nb = (int)cdiv(ctx, 16);
     int32_t* bt = h + M.o_bt + (int64_t)i * maxblk;
@@ -622,12 +625,16 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       tend(ip, 0, 0);
       launches_++;
     } else {
-      // splits per sequence: fill one wave of resident CTAs (4 per SM at the
-      // kernel's register budget) without spilling into a second wave; >= 64
-      // context tokens per split
-      const int64_t base = (int64_t)n * Hkv_;
-      int ns = (int)std::max<int64_t>(1, std::min<int64_t>((4 * 148) / base, cdiv(M.max_ctx, 64)));
-      const int split = (int)cdiv(cdiv(M.max_ctx, ns), 16) * 16;
+      // split size: the largest of 512/256/128 context tokens that still yields
+      // >= 8 CTAs per SM over the batch's actual context lengths (short CTAs of
+      // similar size balance the wave tail; >= 128 tokens amortise a CTA)
+      int split = 512;
+      while (split > 128) {
+        int64_t ctas = 0;
+        for (int i = 0; i < n; ++i) ctas += cdiv(mb_ctx_[i], split);
+        if (ctas * Hkv_ >= 8 * 148) break;
+        split >>= 1;
+      }
       const int ms = (int)cdiv(M.max_ctx, split);
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split,
                           attn_cnt_};
