@@ -132,22 +132,34 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    vals = []
+    vals, secs = [], []
     desc = ""
     for i in range(args.warmup + args.steps):
         v, dt, desc = oracle_sample()
         if i >= args.warmup:
             vals.append(v)
+            secs.append(dt)
     value = statistics.mean(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: Llama-2-7B-shaped random-init, 1 GPU, 256 ShareGPT-length requests",
-                       "parallelism": f"pp{args.gpus}"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_config(args, n_gpus=1):
+    shape = SHAPES[args.model]
+    wl = config_workload(args.config)
+    n_req = len(wl.requests)
+    return {"workload": f"{args.config}: {shape.name}-shaped random-init ({shape.n_layers} layers), {n_req} "
+                        f"ShareGPT-length requests, bucket-predicted lengths, {max(n_gpus, args.stages)}-stage "
+                        f"TD-Pipe ({args.policy})",
+            "model": shape.name, "n_requests": n_req, "global_batch": n_req,
+            "parallelism": f"pp{max(n_gpus, args.stages)}",
+            "l2": "inputs larger than L2 (weights + KV per step >> 126 MB)"}
 
 
 # ---------------------------------------------------------------------- our arm
@@ -233,11 +245,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{args.config}: Llama-2-7B-shaped random-init (32 layers), {n_req} ShareGPT-length "
-                               f"requests, bucket-predicted lengths, {args.stages}-stage TD-Pipe ({args.policy})",
-                   "model": shape.name, "n_requests": n_req, "global_batch": n_req,
-                   "parallelism": f"pp{args.stages}", "l2": "inputs larger than L2 (13.5 GB weights + KV per step)",
-                   "kv_blocks": info["kv_blocks"], "profile_s": round(prof_s, 2)},
+        "config": dict(workload_config(args), kv_blocks=info["kv_blocks"], profile_s=round(prof_s, 2)),
         "bubble_pct": 100.0 * statistics.mean(s["bubble_frac"] for s in kstats) if kstats else None,
         "total_tokens_per_s": sum(s["generated_tokens"] + s["prompt_tokens"] for s in stats) / dev_s,
         "wall_tokens_per_s": gen / wall,
