@@ -16,6 +16,8 @@
 #include <float.h>
 #include <math.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -204,9 +206,247 @@ decode_attn_kernel(DecodeAttnParams p) {
   if (threadIdx.x == 0) p.counters[seq * p.Hkv + kh] = 0;
 }
 
+// ---------------------------------------------------------------- decode v2
+// Page-streaming variant: a producer warp copies whole K and V pages (16 tokens
+// x hd, contiguous in the paged pool) into an R-slot shared-memory ring with
+// cp.async.bulk + mbarrier transaction counts; 4 consumer warps each own every
+// 4th page and compute scores / online softmax / PV from shared memory.  The
+// in-flight bytes live in smem rather than registers, so a few CTAs per SM keep
+// enough of HBM busy even for small batches with long contexts.
+namespace {
+TDP_DEV void dmbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
+}
+TDP_DEV void dmbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+TDP_DEV void dmbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+TDP_DEV void dmbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+TDP_DEV void dbulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+}  // namespace
+
+template <int HD, int G, int R>
+__global__ void __launch_bounds__(160)
+decode_attn_v2_kernel(DecodeAttnParams p) {
+  constexpr int LPT = HD / 8, TPW = 32 / LPT, NWC = 4;
+  constexpr int PAGE = kBlock * HD * 2;            // bytes of one K (or V) page
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint8_t* ring = dsm;                             // R x (K page, V page)
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + R * 2 * PAGE);
+  uint64_t* empty = full + R;
+  float* sm = reinterpret_cast<float*>(empty + R);            // [NWC][G][2]
+  float* sacc = sm + NWC * G * 2;                             // [NWC][G][HD]
+  __shared__ int s_last;
+
+  pdl_trigger();
+  const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
+  const int ctx = p.ctx[seq];
+  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
+  if (split >= n_splits) return;
+  const int t_begin = split * p.split_tokens;
+  const int t_end = min(ctx, t_begin + p.split_tokens);
+  const int pg0 = t_begin >> 4, npg = ((t_end + 15) >> 4) - pg0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.H;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < R; ++i) {
+      dmbar_init(&full[i], 1);
+      dmbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
+  const int64_t head_stride = (int64_t)kBlock * HD;
+
+  if (warp == NWC) {   // producer
+    if (lane == 0) {
+      for (int i = 0; i < npg; ++i) {
+        const int s = i % R;
+        if (i >= R) dmbar_wait(&empty[s], ((i / R) & 1) ^ 1);
+        const int blk = bt[pg0 + i];
+        const bf16* kp = p.kv + (((int64_t)blk * 2) * p.Hkv + kh) * head_stride;
+        dmbar_expect(&full[s], 2 * PAGE);
+        dbulk(ring + s * 2 * PAGE, kp, PAGE, &full[s]);
+        dbulk(ring + s * 2 * PAGE + PAGE, kp + (int64_t)p.Hkv * head_stride, PAGE, &full[s]);
+      }
+    }
+  } else {
+    const int tg = lane / LPT, sub = lane % LPT;
+    const float scale = rsqrtf((float)HD) * kLog2e;
+    float q[G][8], m[G], l[G], acc[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint4 u = *reinterpret_cast<const uint4*>(p.q + ((int64_t)seq * H + kh * G + g) * HD + sub * 8);
+      bf16x8_to_f32(u, q[g]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) q[g][i] *= scale;
+      m[g] = -INFINITY;
+      l[g] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
+    }
+    for (int i = warp; i < npg; i += NWC) {
+      const int s = i % R;
+      dmbar_wait(&full[s], (i / R) & 1);
+      const uint8_t* kpg = ring + s * 2 * PAGE;
+      const uint8_t* vpg = kpg + PAGE;
+      const int tbase = (pg0 + i) << 4;
+#pragma unroll
+      for (int it = 0; it < kBlock / TPW; ++it) {
+        const int r = it * TPW + tg;                 // token row inside the page
+        const bool valid = tbase + r < t_end;
+        float kf[8], vf[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(kpg + (r * HD + sub * 8) * 2), kf);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(vpg + (r * HD + sub * 8) * 2), vf);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float sc = 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) sc = fmaf(q[g][k], kf[k], sc);
+#pragma unroll
+          for (int o = LPT / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+          if (valid) {
+            const float mn = fmaxf(m[g], sc);
+            const float corr = exp2f(m[g] - mn);
+            const float pr = exp2f(sc - mn);
+            l[g] = l[g] * corr + pr;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[g][k] = fmaf(pr, vf[k], acc[g][k] * corr);
+            m[g] = mn;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) dmbar_arrive(&empty[s]);
+    }
+    // merge the token groups of the warp, then the warps through smem
+#pragma unroll
+    for (int o = LPT; o < 32; o <<= 1) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m[g], o);
+        const float l2 = __shfl_xor_sync(0xffffffffu, l[g], o);
+        const float mn = fmaxf(m[g], m2);
+        const float c1 = mn == -INFINITY ? 0.f : exp2f(m[g] - mn);
+        const float c2 = mn == -INFINITY ? 0.f : exp2f(m2 - mn);
+        l[g] = l[g] * c1 + l2 * c2;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float a2 = __shfl_xor_sync(0xffffffffu, acc[g][k], o);
+          acc[g][k] = acc[g][k] * c1 + a2 * c2;
+        }
+        m[g] = mn;
+      }
+    }
+    if (tg == 0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (sub == 0) {
+          sm[(warp * G + g) * 2] = m[g];
+          sm[(warp * G + g) * 2 + 1] = l[g];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sacc[(warp * G + g) * HD + sub * 8 + k] = acc[g][k];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
+    const int g = e / HD, dim = e % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NWC; ++w) M = fmaxf(M, sm[(w * G + g) * 2]);
+    float L = 0.f, A = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWC; ++w) {
+      const float c = M == -INFINITY ? 0.f : exp2f(sm[(w * G + g) * 2] - M);
+      L += sm[(w * G + g) * 2 + 1] * c;
+      A += sacc[(w * G + g) * HD + dim] * c;
+    }
+    const int h = kh * G + g;
+    if (n_splits == 1) {
+      p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
+    } else {
+      float* part = p.part + (((int64_t)seq * H + h) * p.max_splits + split) * (HD + 2);
+      __stcg(part + 2 + dim, A);
+      if (dim == 0) {
+        __stcg(part, M);
+        __stcg(part + 1, L);
+      }
+    }
+  }
+  if (n_splits == 1) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[seq * p.Hkv + kh], 1) == n_splits - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
+    const int g = e / HD, dim = e % HD;
+    const int h = kh * G + g;
+    const float* part = p.part + ((int64_t)seq * H + h) * p.max_splits * (HD + 2);
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < n_splits; ++s2) M = fmaxf(M, __ldcg(part + s2 * (HD + 2)));
+    float L = 0.f, A = 0.f;
+    for (int s2 = 0; s2 < n_splits; ++s2) {
+      const float* ps = part + s2 * (HD + 2);
+      const float c = exp2f(__ldcg(ps) - M);
+      L += __ldcg(ps + 1) * c;
+      A += __ldcg(ps + 2 + dim) * c;
+    }
+    p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
+  }
+  if (threadIdx.x == 0) p.counters[seq * p.Hkv + kh] = 0;
+}
+
+template <int HD, int G>
+static void launch_v2(const DecodeAttnParams& p, cudaStream_t st) {
+  constexpr int R = HD >= 128 ? 6 : 8;
+  constexpr int smem = R * 2 * kBlock * HD * 2 + R * 16 + 4 * G * 2 * 4 + 4 * G * HD * 4 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_attn_v2_kernel<HD, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  launch_k(decode_attn_v2_kernel<HD, G, R>, dim3(p.max_splits, p.Hkv, p.n), dim3(160), smem, st, p);
+}
+
+static bool v2_enabled() {   // TDPIPE_ATTN_V2=0: register-pipelined kernel (A/B)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TDPIPE_ATTN_V2");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <int HD>
 static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
   const int G = p.H / p.Hkv;
+  if (v2_enabled()) {
+    switch (G) {
+      case 1: launch_v2<HD, 1>(p, st); return;
+      case 2: launch_v2<HD, 2>(p, st); return;
+      case 4: launch_v2<HD, 4>(p, st); return;
+      case 8: launch_v2<HD, 8>(p, st); return;
+      default: return;
+    }
+  }
   dim3 grid(p.max_splits, p.Hkv, p.n);
   switch (G) {
     case 1: launch_k(decode_attn_kernel<HD, 1>, grid, dim3(128), 0, st, p); break;
