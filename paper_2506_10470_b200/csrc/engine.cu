@@ -628,11 +628,15 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       // split size: the largest of 512/256/128 context tokens that still yields
       // >= 8 CTAs per SM over the batch's actual context lengths (short CTAs of
       // similar size balance the wave tail; >= 128 tokens amortise a CTA)
+      // (the page-streaming kernel keeps 6 pages in flight per CTA, so it wants
+      // fewer, longer CTAs: one resident wave of ~4 per SM)
+      static const bool v2 = !(getenv("TDPIPE_ATTN_V2") && getenv("TDPIPE_ATTN_V2")[0] == '0');
+      const int64_t target = (v2 ? 4 : 8) * 148;
       int split = 512;
-      while (split > 128) {
+      while (split > (v2 ? 256 : 128)) {
         int64_t ctas = 0;
         for (int i = 0; i < n; ++i) ctas += cdiv(mb_ctx_[i], split);
-        if (ctas * Hkv_ >= 8 * 148) break;
+        if (ctas * Hkv_ >= target) break;
         split >>= 1;
       }
       const int ms = (int)cdiv(M.max_ctx, split);

@@ -237,10 +237,11 @@ TDP_DEV void dbulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
 }
 }  // namespace
 
-template <int HD, int G, int R>
+template <int HD, int G, int RW>
 __global__ void __launch_bounds__(160)
 decode_attn_v2_kernel(DecodeAttnParams p) {
   constexpr int LPT = HD / 8, TPW = 32 / LPT, NWC = 4;
+  constexpr int R = NWC * RW;                      // ring slots (RW per consumer warp)
   constexpr int PAGE = kBlock * HD * 2;            // bytes of one K (or V) page
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring = dsm;                             // R x (K page, V page)
@@ -274,9 +275,13 @@ decode_attn_v2_kernel(DecodeAttnParams p) {
 
   if (warp == NWC) {   // producer
     if (lane == 0) {
+      // page i belongs to consumer warp i % NWC, which owns slots
+      // [w*RW, (w+1)*RW) and consumes them strictly in order (one consumer per
+      // barrier: a parity wait can never be two phases ahead)
       for (int i = 0; i < npg; ++i) {
-        const int s = i % R;
-        if (i >= R) dmbar_wait(&empty[s], ((i / R) & 1) ^ 1);
+        const int w = i % NWC, j = i / NWC;
+        const int s = w * RW + j % RW;
+        if (j >= RW) dmbar_wait(&empty[s], ((j / RW) & 1) ^ 1);
         const int blk = bt[pg0 + i];
         const bf16* kp = p.kv + (((int64_t)blk * 2) * p.Hkv + kh) * head_stride;
         dmbar_expect(&full[s], 2 * PAGE);
@@ -300,8 +305,9 @@ decode_attn_v2_kernel(DecodeAttnParams p) {
       for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
     }
     for (int i = warp; i < npg; i += NWC) {
-      const int s = i % R;
-      dmbar_wait(&full[s], (i / R) & 1);
+      const int j = i / NWC;
+      const int s = warp * RW + j % RW;
+      dmbar_wait(&full[s], (j / RW) & 1);
       const uint8_t* kpg = ring + s * 2 * PAGE;
       const uint8_t* vpg = kpg + PAGE;
       const int tbase = (pg0 + i) << 4;
@@ -416,14 +422,15 @@ decode_attn_v2_kernel(DecodeAttnParams p) {
 
 template <int HD, int G>
 static void launch_v2(const DecodeAttnParams& p, cudaStream_t st) {
-  constexpr int R = HD >= 128 ? 6 : 8;
+  constexpr int RW = 2;
+  constexpr int R = 4 * RW;
   constexpr int smem = R * 2 * kBlock * HD * 2 + R * 16 + 4 * G * 2 * 4 + 4 * G * HD * 4 + 64;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_attn_v2_kernel<HD, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(decode_attn_v2_kernel<HD, G, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  launch_k(decode_attn_v2_kernel<HD, G, R>, dim3(p.max_splits, p.Hkv, p.n), dim3(160), smem, st, p);
+  launch_k(decode_attn_v2_kernel<HD, G, RW>, dim3(p.max_splits, p.Hkv, p.n), dim3(160), smem, st, p);
 }
 
 static bool v2_enabled() {   // TDPIPE_ATTN_V2=0: register-pipelined kernel (A/B)

@@ -207,3 +207,24 @@ def test_llama7b_shaped_bench_launch_config():
         ref = F.sequence_logits(W, seq)
         _rows_ok(out[i], ref[-2])
         _rows_ok(out2[i], ref[-1])
+
+
+def test_decode_attention_long_context_many_pages():
+    """Long contexts (many KV pages per split, every ring slot reused several
+    times) for MHA hd=128 and GQA: decode logits vs the oracle."""
+    for shape in (ModelShape("mha128", 1, 512, 4, 4, 512, 512, max_seq_len=4096),
+                  ModelShape("gqa8_long", 1, 1024, 8, 1, 1024, 512, max_seq_len=4096)):
+        W = OracleWeights(shape)
+        t = TDPipe(shape, 1, kv_blocks=1024)
+        rng = np.random.default_rng(11)
+        lengths = [3000, 1500, 37]
+        prompts = [rng.integers(0, shape.vocab, size=L).astype(np.int32) for L in lengths]
+        bt = _paged([L + 2 for L in lengths])
+        out = t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * 3, lengths, bt, np.concatenate(prompts))
+        nxt = np.argmax(out, -1).astype(np.int32)
+        out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * 3, bt, nxt)
+        t.close()
+        for i, p in enumerate(prompts):
+            ref = F.sequence_logits(W, np.concatenate([p, [nxt[i]]]))
+            _rows_ok(out[i], ref[-2])
+            _rows_ok(out2[i], ref[-1])
