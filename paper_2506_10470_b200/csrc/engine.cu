@@ -630,7 +630,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       // similar size balance the wave tail; >= 128 tokens amortise a CTA)
       // (the page-streaming kernel keeps 6 pages in flight per CTA, so it wants
       // fewer, longer CTAs: one resident wave of ~4 per SM)
-      static const bool v2 = !(getenv("TDPIPE_ATTN_V2") && getenv("TDPIPE_ATTN_V2")[0] == '0');
+      static const bool v2 = getenv("TDPIPE_ATTN_V2") && getenv("TDPIPE_ATTN_V2")[0] == '1';
       const int64_t target = (v2 ? 4 : 8) * 148;
       int split = 512;
       while (split > (v2 ? 256 : 128)) {

@@ -433,11 +433,11 @@ static void launch_v2(const DecodeAttnParams& p, cudaStream_t st) {
   launch_k(decode_attn_v2_kernel<HD, G, RW>, dim3(p.max_splits, p.Hkv, p.n), dim3(160), smem, st, p);
 }
 
-static bool v2_enabled() {   // TDPIPE_ATTN_V2=0: register-pipelined kernel (A/B)
+static bool v2_enabled() {   // TDPIPE_ATTN_V2=1: smem page-ring kernel (measured slower; A/B only)
   static int on = -1;
   if (on < 0) {
     const char* e = std::getenv("TDPIPE_ATTN_V2");
-    on = (e && e[0] == '0') ? 0 : 1;
+    on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }
