@@ -225,16 +225,26 @@ td_status td_get_timing(struct td_ctx* ctx, const char* name, int64_t* launches,
  * 1 = mma.sync baseline; splits > 1 exercises the split-K reduction.  Runs on
  * `device`, allocates and frees its own buffers, synchronous.  impl 0 packs W
  * into the tile-packed layout the engine uses; impl 2 = tcgen05 with row-major
- * W through a TMA descriptor. */
+ * W through a TMA descriptor; impl 3 = the stream-K decode kernel (T <= 128,
+ * packed W). */
 td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N, int32_t K,
                        int32_t impl, int32_t splits, float* out);
 
 /* GEMM timing sweep (testing only): average device microseconds per call of
  * the tcgen05 GEMM on [T, K] x [N, K]^T (tile-packed weights, fp32 output),
  * cycling over `copies` weight buffers so that the weights stream from HBM;
- * splits = split-K count (1 = none); decode = 1 selects decode token tiles. */
+ * splits = split-K count (1 = none); decode = 1 selects decode token tiles,
+ * decode = 2 the stream-K decode kernel (T <= 128). */
 td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t splits, int32_t decode,
                         int32_t iters, int32_t copies, float* us_per_call);
+
+/* Decode-attention timing sweep (testing only): average device microseconds
+ * per decode-attention launch for n sequences of context lengths ctx[n] (host),
+ * H query / Hkv kv heads of size hd, pages scattered through a pool rotated
+ * over enough copies (<= 400 MiB) that K/V stream from HBM, launched with
+ * the engine's plan.  K/V, q are zeros (timing only). */
+td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx, int32_t H, int32_t Hkv, int32_t hd,
+                        int32_t iters, float* us_per_call);
 
 /* Generate the two ncclUniqueIds (256 bytes) rank 0 shares with all ranks. */
 td_status td_nccl_ids(void* out256);

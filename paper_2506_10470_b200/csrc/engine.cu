@@ -197,6 +197,7 @@ class CudaEngine : public Engine {
 };
 
 enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
+constexpr int kSkTicketOff = 1 << 15;   // counters_[kSkTicketOff ..]: stream-K GEMM tile tickets
 constexpr int kDecOff = 8;   // decode-phase GEMM classes = prefill class + kDecOff
 constexpr int kAttnBucket = 15, kGemmBucket = 19;   // + bucket(n): batch-size buckets for decode
 static inline int bucket_of(int n) { return n <= 8 ? 0 : n <= 32 ? 1 : n <= 128 ? 2 : 3; }
@@ -474,6 +475,10 @@ td_status CudaEngine::make_x_ops() {
 // consumes the partials (launch_resid_norm).
 int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
                      bool defer) {
+  if (gemm_sk_applies(W, T, decode)) {   // stream-K weight streaming, epilogue applied in-kernel
+    launches_ += 1;
+    return launch_gemm_sk(W, xo.by_bn, T, ep, ws_, counters_ + kSkTicketOff, st_);
+  }
   int splits = 1;
   // 129..256-token decode batches of the wide GEMMs (QKV, gate/up, LM head) are
   // closer to the tensor roof than to HBM: take the token-major kernel
@@ -625,23 +630,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       tend(ip, 0, 0);
       launches_++;
     } else {
-      // split size: the largest of 512/256/128 context tokens that still yields
-      // >= 8 CTAs per SM over the batch's actual context lengths (short CTAs of
-      // similar size balance the wave tail; >= 128 tokens amortise a CTA)
-      // (the page-streaming kernel keeps 6 pages in flight per CTA, so it wants
-      // fewer, longer CTAs: one resident wave of ~4 per SM)
-      static const bool v2 = getenv("TDPIPE_ATTN_V2") && getenv("TDPIPE_ATTN_V2")[0] == '1';
-      const int64_t target = (v2 ? 4 : 8) * 148;
-      int split = 512;
-      while (split > (v2 ? 256 : 128)) {
-        int64_t ctas = 0;
-        for (int i = 0; i < n; ++i) ctas += cdiv(mb_ctx_[i], split);
-        if (ctas * Hkv_ >= target) break;
-        split >>= 1;
-      }
-      const int ms = (int)cdiv(M.max_ctx, split);
-      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, ms, n, H_, Hkv_, hd_, split,
+      DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, n, H_, Hkv_, hd_, 0,
                           attn_cnt_};
+      plan_decode_attn(dp, mb_ctx_.data());
       const int ida = tbegin(cDecAttn);
       if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
       launch_decode_attn(dp, st_);

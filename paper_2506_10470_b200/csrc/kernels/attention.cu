@@ -16,6 +16,7 @@
 #include <float.h>
 #include <math.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -29,101 +30,18 @@ struct SoftmaxState {
   float m, l;
 };
 
+// Combine the per-thread online-softmax states of one CTA (lanes, then warps)
+// and write the result: o directly for a single segment, else the segment's
+// partial (m, l, acc) -- the last segment of (seq, kh) to arrive merges all
+// partials in segment order (deterministic; no separate combine launch).
 template <int HD, int G>
-__global__ void __launch_bounds__(128)
-decode_attn_kernel(DecodeAttnParams p) {
-  constexpr int LPT = HD / 8;          // lanes per token
-  constexpr int TPW = 32 / LPT;        // tokens per warp per step
+__device__ __forceinline__ void attn_finish(const DecodeAttnParams& p, int seq, int kh, int split, int n_splits,
+                                            float (&m)[G], float (&l)[G], float (&acc)[G][8]) {
+  constexpr int LPT = HD / 8;
   constexpr int NW = 4;
-  constexpr int U = 4;                 // tokens in flight per thread group
-  pdl_trigger();
-  pdl_wait();
-  const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
-  const int ctx = p.ctx[seq];
-  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
-  if (split >= n_splits) return;
-  const int t_begin = split * p.split_tokens;
-  const int t_end = min(ctx, t_begin + p.split_tokens);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tg = lane / LPT, sub = lane % LPT;
   const int H = p.H;
-  const float scale = rsqrtf((float)HD) * kLog2e;
-
-  float q[G][8];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p.q + ((int64_t)seq * H + kh * G + g) * HD + sub * 8);
-    bf16x8_to_f32(u, q[g]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) q[g][i] *= scale;
-  }
-  float m[G], l[G], acc[G][8];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m[g] = -INFINITY;
-    l[g] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
-  }
-  const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
-  const int64_t head_stride = (int64_t)kBlock * HD;           // one (blk, kv, head) page
-  constexpr int STEP = NW * TPW * U;
-  // software pipeline (G <= 2): the next step's K/V loads are in flight while
-  // this step's softmax runs (two steps of 16-byte loads per thread)
-  constexpr bool PF = G <= 2;
-  uint4 kr[U], vr[U], kn[U], vn[U];
-  bool valid[U], vnx[U];
-  auto issue = [&](int base, uint4* K, uint4* Vv, bool* ok) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = base + (u * NW + warp) * TPW + tg;
-      ok[u] = t < t_end;
-      const int tt = ok[u] ? t : t_begin;
-      const int blk = bt[tt >> 4];
-      const int64_t kb = (((int64_t)blk * 2) * p.Hkv + kh) * head_stride + (tt & 15) * HD + sub * 8;
-      K[u] = ld_nc_v4(p.kv + kb);
-      Vv[u] = ld_nc_v4(p.kv + kb + (int64_t)p.Hkv * head_stride);
-    }
-  };
-  issue(t_begin, kr, vr, valid);
-  for (int base = t_begin; base < t_end; base += STEP) {
-    if (PF && base + STEP < t_end) issue(base + STEP, kn, vn, vnx);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      float kf[8], vf[8];
-      bf16x8_to_f32(kr[u], kf);
-      bf16x8_to_f32(vr[u], vf);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s = fmaf(q[g][i], kf[i], s);
-#pragma unroll
-        for (int o = LPT / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (valid[u]) {
-          const float mn = fmaxf(m[g], s);
-          const float corr = exp2f(m[g] - mn);
-          const float pr = exp2f(s - mn);
-          l[g] = l[g] * corr + pr;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[g][i] = fmaf(pr, vf[i], acc[g][i] * corr);
-          m[g] = mn;
-        }
-      }
-    }
-    if (base + STEP < t_end) {
-      if (PF) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          kr[u] = kn[u];
-          vr[u] = vn[u];
-          valid[u] = vnx[u];
-        }
-      } else {
-        issue(base + STEP, kr, vr, valid);
-      }
-    }
-  }
   // merge thread groups within the warp (lanes with equal `sub`)
 #pragma unroll
   for (int o = LPT; o < 32; o <<= 1) {
@@ -145,6 +63,7 @@ decode_attn_kernel(DecodeAttnParams p) {
   }
   __shared__ float sm[NW][G][2];
   __shared__ float sacc[NW][G][HD];
+  __syncthreads();   // the previous segment of this CTA is done with sm / sacc
   if (tg == 0) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -204,6 +123,133 @@ decode_attn_kernel(DecodeAttnParams p) {
     p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
   }
   if (threadIdx.x == 0) p.counters[seq * p.Hkv + kh] = 0;
+}
+
+
+// One CTA attends (sequence seq, kv head kh) over context tokens
+// [t_begin, t_end): segment `split` of `n_splits`.  With n_splits == 1 it writes
+// o; otherwise it writes the segment's partial (m, l, acc) and the last
+// segment to finish merges all of them in segment order.
+template <int HD, int G>
+__device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq, int kh, int t_begin, int t_end,
+                                             int split, int n_splits, int newest) {
+  constexpr int LPT = HD / 8;          // lanes per token
+  constexpr int TPW = 32 / LPT;        // tokens per warp per step
+  constexpr int NW = 4;
+  constexpr int U = 4;                 // tokens in flight per thread group
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tg = lane / LPT, sub = lane % LPT;
+  const int H = p.H;
+  const float scale = rsqrtf((float)HD) * kLog2e;
+
+  float m[G], l[G], acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
+  }
+  const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
+  const int64_t head_stride = (int64_t)kBlock * HD;           // one (blk, kv, head) page
+  constexpr int STEP = NW * TPW * U;
+  // software pipeline (G <= 2): the next step's K/V loads are in flight while
+  // this step's softmax runs (two steps of 16-byte loads per thread)
+  constexpr bool PF = G <= 2;
+  uint4 kr[U], vr[U], kn[U], vn[U];
+  bool valid[U], vnx[U];
+  auto issue = [&](int base, uint4* K, uint4* Vv, bool* ok) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + (u * NW + warp) * TPW + tg;
+      ok[u] = t < t_end;
+      const int tt = ok[u] ? t : t_begin;
+      const int blk = bt[tt >> 4];
+      const int64_t kb = (((int64_t)blk * 2) * p.Hkv + kh) * head_stride + (tt & 15) * HD + sub * 8;
+      K[u] = ld_nc_v4(p.kv + kb);
+      Vv[u] = ld_nc_v4(p.kv + kb + (int64_t)p.Hkv * head_stride);
+    }
+  };
+  // The first step's K/V loads go out before the PDL wait: every context
+  // token except the newest was written by earlier steps, so they overlap the
+  // tail of the QKV kernel.  After the wait, the thread holding the newest
+  // token (written by that kernel) reloads it through L2 (ld.cg: the
+  // pre-wait load may have left a stale line in L1), and q is read.
+  issue(t_begin, kr, vr, valid);
+  pdl_wait();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int t = t_begin + (u * NW + warp) * TPW + tg;
+    if (t == newest) {
+      const int64_t kb = (((int64_t)bt[t >> 4] * 2) * p.Hkv + kh) * head_stride + (t & 15) * HD + sub * 8;
+      kr[u] = __ldcg(reinterpret_cast<const uint4*>(p.kv + kb));
+      vr[u] = __ldcg(reinterpret_cast<const uint4*>(p.kv + kb + (int64_t)p.Hkv * head_stride));
+    }
+  }
+  float q[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p.q + ((int64_t)seq * H + kh * G + g) * HD + sub * 8);
+    bf16x8_to_f32(u, q[g]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[g][i] *= scale;
+  }
+  for (int base = t_begin; base < t_end; base += STEP) {
+    if (PF && base + STEP < t_end) issue(base + STEP, kn, vn, vnx);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float kf[8], vf[8];
+      bf16x8_to_f32(kr[u], kf);
+      bf16x8_to_f32(vr[u], vf);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s = fmaf(q[g][i], kf[i], s);
+#pragma unroll
+        for (int o = LPT / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (valid[u]) {
+          const float mn = fmaxf(m[g], s);
+          const float corr = exp2f(m[g] - mn);
+          const float pr = exp2f(s - mn);
+          l[g] = l[g] * corr + pr;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[g][i] = fmaf(pr, vf[i], acc[g][i] * corr);
+          m[g] = mn;
+        }
+      }
+    }
+    if (base + STEP < t_end) {
+      if (PF) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          kr[u] = kn[u];
+          vr[u] = vn[u];
+          valid[u] = vnx[u];
+        }
+      } else {
+        issue(base + STEP, kr, vr, valid);
+      }
+    }
+  }
+  attn_finish<HD, G>(p, seq, kh, split, n_splits, m, l, acc);
+}
+
+template <int HD, int G>
+__global__ void __launch_bounds__(128)
+decode_attn_kernel(DecodeAttnParams p) {
+  pdl_trigger();
+  // ctx / block tables are host-uploaded metadata (complete before the
+  // previous kernel ran): read before the PDL wait, which attend_range takes
+  const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
+  const int ctx = p.ctx[seq];
+  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
+  if (split >= n_splits) {
+    pdl_wait();
+    return;
+  }
+  const int t_begin = split * p.split_tokens;
+  attend_range<HD, G>(p, seq, kh, t_begin, min(ctx, t_begin + p.split_tokens), split, n_splits, ctx - 1);
 }
 
 // ---------------------------------------------------------------- decode v2
@@ -463,6 +509,26 @@ static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
     default: return;
   }
 
+}
+
+void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
+  // split size: the largest of 512/256/128 context tokens that still yields
+  // >= 8 CTAs per SM over the batch's actual context lengths (short CTAs of
+  // similar size balance the wave tail; >= 128 tokens amortise a CTA); the
+  // page-ring kernel keeps 6 pages in flight per CTA, so it wants fewer,
+  // longer CTAs: one resident wave of ~4 per SM
+  const bool v2 = v2_enabled();
+  const int64_t target = (v2 ? 4 : 8) * 148;
+  int split = 512, max_ctx = 1;
+  for (int i = 0; i < p.n; ++i) max_ctx = std::max(max_ctx, ctx[i]);
+  for (;;) {
+    int64_t ctas = 0;
+    for (int i = 0; i < p.n; ++i) ctas += (ctx[i] + split - 1) / split;
+    if (ctas * p.Hkv >= target || split <= (v2 ? 256 : 128)) break;
+    split >>= 1;
+  }
+  p.split_tokens = split;
+  p.max_splits = (max_ctx + split - 1) / split;
 }
 
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {

@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -546,6 +547,242 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
   }
 }
 
+// ----------------------------------------------------------------------------
+// Stream-K decode GEMM (swap-AB, T <= BN <= 128 tokens, one token tile).
+// The U = (Nf/128) x (K/64) k-blocks of the weight matrix, in (row tile,
+// k-block) order, are cut into P = min(148, U) contiguous ranges of equal size,
+// one persistent CTA per SM: every SM streams the same number of weight bytes,
+// with no wave tail and no per-tile ramp (the TMA ring runs continuously
+// across tiles; two TMEM accumulators let the epilogue of one segment overlap
+// the MMAs of the next).  A row tile cut by range boundaries has 2+
+// contributors; each writes its fp32 partial [BN][128] to ws and takes a
+// ticket, and the last to arrive sums all partials in contributor order
+// (deterministic) and applies the fused epilogue.  Nothing ever waits on
+// another CTA, so the kernel cannot deadlock whatever the residency.  The
+// owner of a cut tile (the CTA holding its k-block 0) reaches it last in its
+// range, so it usually finds every other partial in place and skips writing
+// its own.
+TDP_DEV int sk_lo(int c, int U, int P) { return (int)(((int64_t)c * U) / P); }
+TDP_DEV int sk_cta_of(int u, int U, int P) {   // the CTA whose range holds k-block u
+  int c = (int)(((int64_t)u * P) / U);
+  while (c + 1 < P && sk_lo(c + 1, U, P) <= u) ++c;
+  while (c > 0 && sk_lo(c, U, P) > u) --c;
+  return c;
+}
+TDP_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+gemm_sk_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int KB,
+               EpiParams ep, float* __restrict__ ws, int* __restrict__ tickets) {
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * (BN < 32 ? 32 : BN);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int s_last[2];
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MT = (Nf + 127) >> 7;
+  const int U = MT * KB, P = gridDim.x, c = blockIdx.x;
+  const int lo = sk_lo(c, U, P), hi = sk_lo(c + 1, U, P);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights do not depend on the previous kernel: the first stages stream
+      // before the PDL wait, the activation tiles after it
+      const uint64_t pol = policy_evict_first();
+      const int n = hi - lo;
+      const int pre = min(n, STAGES);
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], STAGE_BYTES);
+        bulk_load(smem + i * STAGE_BYTES, wpk + ((int64_t)(lo + i) << 13), A_BYTES, &full[i], pol);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(smem + i * STAGE_BYTES + A_BYTES, &tmX, ((lo + i) % KB) * BK, 0, &full[i]);
+      for (int i = pre; i < n; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        // packed weights: k-block u of the flattened (row tile, k-block) order
+        // is the u-th 16 KB tile
+        bulk_load(sa, wpk + ((int64_t)(lo + i) << 13), A_BYTES, &full[s], pol);
+        tma_load_2d(sa + A_BYTES, &tmX, ((lo + i) % KB) * BK, 0, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      int i = 0, seg = 0;
+      for (int u = lo; u < hi; ++seg) {
+        const int mt = u / KB;
+        const int end = min(hi, (mt + 1) * KB);
+        const int a = seg & 1;
+        if (seg >= 2) mbar_wait(&tempty[a], ((uint32_t)(seg >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(a * BN);
+        for (int u0 = u; u < end; ++u, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
+          tc_fence_after();
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          const uint64_t ad = smem_desc_sw128(sa);
+          const uint64_t bd = smem_desc_sw128(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_f16(acc, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (u != u0 || k != 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[a]);
+      }
+    }
+  } else {
+    pdl_wait();
+    const int q = warp & 3;
+    const int et = threadIdx.x - 64;            // 0..127 over the epilogue warps
+    const int nch = (T + 31) >> 5;
+    int seg = 0;
+    for (int u = lo; u < hi; ++seg) {
+      const int mt = u / KB;
+      const int kb_a = u - mt * KB;
+      const int end = min(hi, (mt + 1) * KB);
+      u = end;
+      const int a = seg & 1;
+      mbar_wait(&tfull[a], (uint32_t)(seg >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t tacc = tmem + (uint32_t)(a * BN) + ((uint32_t)(q * 32) << 16);
+      const int f = mt * 128 + q * 32 + lane;
+      const bool whole = kb_a == 0 && end - mt * KB == KB;
+      if (whole) {
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+          uint32_t r[32];
+          tmem_ld32(tacc + (uint32_t)(ch * 32), r);
+          epilogue_chunk(ep, T, Nf, f, ch * 32, r);
+        }
+      } else {
+        const int c0 = sk_cta_of(mt * KB, U, P), c1 = sk_cta_of(mt * KB + KB - 1, U, P);
+        const int n = c1 - c0 + 1;
+        const bool owner = c == c0;
+        // partial slots: 2c = a non-owner's (its first segment), 2c+1 = the owner's
+        const int my_slot = owner ? 2 * c + 1 : 2 * c;
+        auto write_partial = [&]() {
+          float* wp = ws + ((int64_t)my_slot * BN) * 128 + q * 32 + lane;
+#pragma unroll 1
+          for (int ch = 0; ch < nch; ++ch) {
+            uint32_t r[32];
+            tmem_ld32(tacc + (uint32_t)(ch * 32), r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (ch * 32 + j < T) __stcg(wp + (ch * 32 + j) * 128, __uint_as_float(r[j]));
+          }
+        };
+        int last = 0;
+        if (owner) {
+          if (et == 0) s_last[a] = ld_acquire(tickets + mt) == n - 1;
+          named_bar_sync(1, 128);
+          last = s_last[a];
+          named_bar_sync(1, 128);
+        }
+        if (!last) {
+          write_partial();
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (et == 0) s_last[a] = atomicAdd(tickets + mt, 1) == n - 1;
+          named_bar_sync(1, 128);
+          last = s_last[a];
+        }
+        if (last) {
+          __threadfence();
+          if (et == 0) tickets[mt] = 0;
+#pragma unroll 1
+          for (int ch = 0; ch < nch; ++ch) {
+            uint32_t r[32];
+            tmem_ld32(tacc + (uint32_t)(ch * 32), r);
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            for (int cc = c0; cc <= c1; ++cc) {   // contributor order: deterministic sum
+              if (cc == c) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+              } else {
+                const float* rp = ws + ((int64_t)(cc == c0 ? 2 * cc + 1 : 2 * cc) * BN + ch * 32) * 128 + q * 32 + lane;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] += ch * 32 + j < T ? __ldcg(rp + j * 128) : 0.f;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+            epilogue_chunk(ep, T, Nf, f, ch * 32, r);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+template <int BN, int STAGES>
+void launch_sk(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, float* ws, int* tickets,
+               cudaStream_t st) {
+  auto kern = gemm_sk_kernel<BN, STAGES>;
+  constexpr int sm = STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    attr = true;
+  }
+  const int KB = W.K / BK;
+  const int U = ((W.rows + 127) / 128) * KB;
+  launch_k(kern, dim3(std::min(U, kSkCtas)), dim3(192), sm, st, X.map, W.base, W.rows, T, KB, ep, ws, tickets);
+}
+
 // split-K reduction: sums the partials in split order (deterministic) and
 // applies the fused epilogue; grid-stride over (token, feature pair)
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int Nf, EpiParams ep) {
@@ -681,6 +918,38 @@ static bool tn_enabled() {   // TDPIPE_TN=0: prefill through the swap-AB kernel 
     on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
+}
+
+// TDPIPE_SKGEMM=1 routes decode GEMMs (T <= 128) through the stream-K kernel.
+// Off by default: the isolated sweep (profiles/r1/gemm_sk_sweep.txt) measures
+// it 2-3 us slower per call than the split-K grid at every decode shape (the
+// owner's fix-up of a cut tile adds a dependent L2 round trip at the end of
+// the range, and a full-SM persistent grid leaves no room for the next
+// kernel's PDL prologue).
+static bool sk_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TDPIPE_SKGEMM");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+bool gemm_sk_applies(const TcOperand& W, int T, bool decode) {
+  return decode && W.packed && T <= 128 && sk_enabled();
+}
+
+int launch_gemm_sk(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, float* ws, int* tickets,
+                   cudaStream_t st) {
+  if (T <= 0) return 1;
+  switch (tc_bn_for(T, true)) {
+    // one CTA per SM with <= 110 KB of smem, so that the next kernel's CTAs
+    // can start (PDL) and prefetch beside it
+    case 32: launch_sk<32, 5>(W, Xby_bn[0], T, ep, ws, tickets, st); break;
+    case 64: launch_sk<64, 4>(W, Xby_bn[1], T, ep, ws, tickets, st); break;
+    default: launch_sk<128, 3>(W, Xby_bn[2], T, ep, ws, tickets, st); break;
+  }
+  return 1;
 }
 
 int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,

@@ -83,6 +83,9 @@ struct DecodeAttnParams {
   int* counters;         // [n * Hkv] zero-initialised split tickets (reset by the merging CTA)
 };
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
+// Launch plan from the host copy of the context lengths: sets split_tokens
+// and max_splits (part[] must hold cdiv(max_seq_len, 128) splits per head).
+void plan_decode_attn(DecodeAttnParams& p, const int* ctx_host);
 
 // Prefill: varlen causal over each sequence's own (paged) K/V.
 struct PrefillAttnParams {

@@ -1,6 +1,7 @@
 // test_entry.cu -- td_test_gemm: kernel-level unit-test entry point (testing only).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "../../include/tdpipe.h"
@@ -22,7 +23,8 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
   cudaStreamCreate(&s);
   if (cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dW, (size_t)N * K * 2) ||
       cudaMalloc(&dO, (size_t)T * N * 4) ||
-      cudaMalloc(&ws, (size_t)std::max(splits, 1) * (Tcap + 256) * ((N + 127) / 128 * 128) * 4) ||
+      cudaMalloc(&ws, std::max<size_t>((size_t)std::max(splits, 1) * (Tcap + 256) * ((N + 127) / 128 * 128),
+                                        (size_t)kSkWsFloats) * 4) ||
       cudaMalloc(&cnt, 65536 * sizeof(int))) {
     st = TD_ENOMEM;
   } else {
@@ -41,7 +43,7 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
       TcOperand w, x[4];
       bool ok = true;
       bf16* dP = nullptr;
-      if (impl == 0) {
+      if (impl == 0 || impl == 3) {
         const int Np = (N + 127) / 128 * 128;
         std::vector<uint16_t> pk((size_t)Np * K, 0);
         for (int r = 0; r < N; ++r)
@@ -54,6 +56,7 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
       }
       for (int i = 0; i < 4; ++i) ok = ok && make_tc_operand(&x[i], dA, Tcap, K, 32 << i);
       if (!ok) st = TD_ECUDA;
+      else if (impl == 3) launch_gemm_sk(w, x, T, ep, ws, cnt, s);
       else launch_gemm_tc(w, x, T, ep, splits, ws, cnt, splits > 1, s);
       cudaStreamSynchronize(s);
       cudaFree(dP);
@@ -86,7 +89,8 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
   for (auto& w : Ws)
     if (cudaMalloc(&w, (size_t)Np * K * 2) != cudaSuccess) st = TD_ENOMEM;
   if (st || cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dO, (size_t)T * N * 4) ||
-      cudaMalloc(&ws, (size_t)std::max(splits, 1) * (Tcap + 256) * Np * 4) || cudaMalloc(&cnt, 65536 * 4)) {
+      cudaMalloc(&ws, std::max<size_t>((size_t)std::max(splits, 1) * (Tcap + 256) * Np, (size_t)kSkWsFloats) * 4) ||
+      cudaMalloc(&cnt, 65536 * 4)) {
     st = TD_ENOMEM;
   } else {
     for (auto& w : Ws) cudaMemset(w, 0, (size_t)Np * K * 2);
@@ -104,12 +108,16 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
     if (!ok) {
       st = TD_ECUDA;
     } else {
-      for (int i = 0; i < 3; ++i) launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode != 0, s);
+      auto call = [&](int i) {
+        if (decode == 2) launch_gemm_sk(w[i % copies], x, T, ep, ws, cnt, s);
+        else launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode != 0, s);
+      };
+      for (int i = 0; i < 3; ++i) call(i);
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       cudaEventRecord(a, s);
-      for (int i = 0; i < iters; ++i) launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode != 0, s);
+      for (int i = 0; i < iters; ++i) call(i);
       cudaEventRecord(b, s);
       if (cudaEventSynchronize(b) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
       float ms = 0;
@@ -124,6 +132,86 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
   cudaFree(dO);
   cudaFree(ws);
   cudaFree(cnt);
+  cudaStreamDestroy(s);
+  return st;
+}
+
+// Decode-attention timing sweep: n sequences with context lengths ctx[] (host),
+// pages scattered through the pool the way the block allocator hands them out;
+// iterations rotate over `copies` disjoint page sets so the K/V stream from HBM.
+extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx, int32_t H, int32_t Hkv, int32_t hd,
+                                   int32_t iters, float* us_per_call) {
+  if (n < 1 || !ctx || H < 1 || Hkv < 1 || H % Hkv || iters < 1 || !us_per_call) return TD_EINVAL;
+  if (hd != 16 && hd != 32 && hd != 64 && hd != 128) return TD_EINVAL;
+  const int G = H / Hkv;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return TD_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
+  int maxblk = 1, max_ctx = 1;
+  int64_t nblk = 0;
+  for (int i = 0; i < n; ++i) {
+    if (ctx[i] < 1) return TD_EINVAL;
+    maxblk = std::max(maxblk, (ctx[i] + 15) / 16);
+    max_ctx = std::max(max_ctx, ctx[i]);
+    nblk += (ctx[i] + 15) / 16;
+  }
+  const int64_t blk_bytes = 2LL * Hkv * 16 * hd * 2;
+  const int copies = (int)std::min<int64_t>(64, std::max<int64_t>(1, (400LL << 20) / (nblk * blk_bytes)));
+  const int64_t pool = nblk * copies;
+  // block tables: a fixed pseudo-random permutation of the pool
+  std::vector<int32_t> perm(pool);
+  for (int64_t i = 0; i < pool; ++i) perm[i] = (int32_t)i;
+  uint64_t x = 0x9E3779B97F4A7C15ull;
+  for (int64_t i = pool - 1; i > 0; --i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    std::swap(perm[i], perm[x % (uint64_t)(i + 1)]);
+  }
+  std::vector<int32_t> bt((size_t)copies * n * maxblk, 0);
+  int64_t k = 0;
+  for (int c = 0; c < copies; ++c)
+    for (int i = 0; i < n; ++i)
+      for (int b = 0; b < (ctx[i] + 15) / 16; ++b) bt[((size_t)c * n + i) * maxblk + b] = perm[k++];
+  const int cap = (max_ctx + 127) / 128;
+  bf16 *kv = nullptr, *q = nullptr, *o = nullptr;
+  float* part = nullptr;
+  int32_t *dctx = nullptr, *dbt = nullptr;
+  int* cnt = nullptr;
+  td_status st = TD_OK;
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  if (cudaMalloc(&kv, pool * blk_bytes) || cudaMalloc(&q, (size_t)n * H * hd * 2) ||
+      cudaMalloc(&o, (size_t)n * H * hd * 2) || cudaMalloc(&part, (size_t)n * H * cap * (hd + 2) * 4) ||
+      cudaMalloc(&dctx, n * 4) || cudaMalloc(&dbt, bt.size() * 4) ||
+      cudaMalloc(&cnt, (size_t)n * Hkv * 4)) {
+    st = TD_ENOMEM;
+  } else {
+    cudaMemset(kv, 0, pool * blk_bytes);
+    cudaMemset(q, 0, (size_t)n * H * hd * 2);
+    cudaMemset(cnt, 0, (size_t)n * Hkv * 4);
+    cudaMemcpy(dctx, ctx, n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice);
+    DecodeAttnParams p{q, kv, dctx, dbt, maxblk, o, part, 0, n, H, Hkv, hd, 0, cnt};
+    plan_decode_attn(p, ctx);
+    auto run = [&](int i) {
+      DecodeAttnParams pi = p;
+      pi.bt = dbt + (size_t)(i % copies) * n * maxblk;
+      launch_decode_attn(pi, s);
+    };
+    for (int i = 0; i < 3; ++i) run(i);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    for (int i = 0; i < iters; ++i) run(i);
+    cudaEventRecord(b, s);
+    if (cudaEventSynchronize(b) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    *us_per_call = ms * 1000.f / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  cudaFree(kv); cudaFree(q); cudaFree(o); cudaFree(part);
+  cudaFree(dctx); cudaFree(dbt); cudaFree(cnt);
   cudaStreamDestroy(s);
   return st;
 }

@@ -63,7 +63,7 @@ class td_batch(C.Structure):
 EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td_submit", "td_upload",
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
-           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_simulate", "td_write_trace"]
+           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                   P(C.c_double)]
     lib.td_nccl_ids.argtypes = [C.c_void_p]
     lib.td_bench_gemm.argtypes = [C.c_int32] * 8 + [P(C.c_float)]
+    lib.td_bench_attn.argtypes = [C.c_int32, C.c_int32, P(C.c_int32)] + [C.c_int32] * 4 + [P(C.c_float)]
     lib.td_simulate.argtypes = [C.c_void_p, P(td_run_stats), C.c_int64]
     lib.td_write_trace.argtypes = [C.c_void_p, C.c_char_p]
     lib.td_test_gemm.argtypes = [C.c_int32, P(C.c_uint16), P(C.c_uint16), C.c_int32, C.c_int32, C.c_int32,
@@ -307,4 +308,15 @@ def td_bench_gemm(T: int, N: int, K: int, splits: int = 1, decode: bool = True, 
     st = lib().td_bench_gemm(device, T, N, K, splits, int(decode), iters, copies, C.byref(us))
     if st != TD_OK:
         raise TDError(f"td_bench_gemm failed: {st}")
+    return us.value
+
+
+def td_bench_attn(ctx, H: int, Hkv: int, hd: int, iters: int = 50, device: int = 0) -> float:
+    """Average device microseconds per decode-attention launch over context
+    lengths `ctx` (the engine's launch plan)."""
+    c = np.ascontiguousarray(ctx, dtype=np.int32)
+    us = C.c_float(0)
+    st = lib().td_bench_attn(device, len(c), _ptr(c, C.c_int32), H, Hkv, hd, iters, C.byref(us))
+    if st != TD_OK:
+        raise TDError(f"td_bench_attn failed: {st}")
     return us.value
