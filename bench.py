@@ -162,6 +162,17 @@ def workload_config(args, n_gpus=1):
             "l2": "inputs larger than L2 (weights + KV per step >> 126 MB)"}
 
 
+def _traffic_record(kernel):
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*",
+                                          f"traffic_{kernel}.json")))
+    if not files:
+        return None
+    rec = json.load(open(files[-1]))
+    rec["file"] = os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))
+    return rec
+
+
 # ---------------------------------------------------------------------- our arm
 def run_ours(args):
     import paper_2506_10470_b200 as tp
@@ -280,6 +291,14 @@ def run_ours(args):
             line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"],
                                 "unit": "GB/s", "frac": round(ach / peaks["hbm"], 4), "traffic": None,
                                 "peak_src": peaks["src"]}
+            # DRAM bytes per launch measured by ncu over every launch of this
+            # kernel in one C2 job (scripts/traffic_attn.py), next to the
+            # algorithmic bytes per launch the engine counted for the same job
+            tf = _traffic_record(dom)
+            if tf:
+                line["roofline"].update(traffic=round(tf["dram_bytes_per_launch"]),
+                                        traffic_algorithmic=round(tf["algorithmic_bytes_per_launch"]),
+                                        traffic_ratio=round(tf["ratio"], 4), traffic_src=tf["file"])
         line["kernels"] = rl
         line["kernel_share"] = share
     if not args.no_cpu_baseline:

@@ -417,7 +417,7 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&ob_, T * H_ * hd_ * 2));
   CK(cudaMalloc(&h_, T * F_ * 2));
   CK(cudaMalloc(&logits_, n * V_ * 4));
-  max_splits_cap_ = (int)cdiv(s_.max_seq_len, 128);
+  max_splits_cap_ = (int)cdiv(s_.max_seq_len, kAttnMinSplit);
   CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
   cudaFree(attn_cnt_);
   CK(cudaMalloc(&attn_cnt_, n * Hkv_ * sizeof(int)));

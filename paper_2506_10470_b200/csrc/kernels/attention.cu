@@ -524,7 +524,7 @@ void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
   for (;;) {
     int64_t ctas = 0;
     for (int i = 0; i < p.n; ++i) ctas += (ctx[i] + split - 1) / split;
-    if (ctas * p.Hkv >= target || split <= (v2 ? 256 : 128)) break;
+    if (ctas * p.Hkv >= target || split <= (v2 ? 256 : kAttnMinSplit)) break;
     split >>= 1;
   }
   p.split_tokens = split;

@@ -84,7 +84,9 @@ struct DecodeAttnParams {
 };
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 // Launch plan from the host copy of the context lengths: sets split_tokens
-// and max_splits (part[] must hold cdiv(max_seq_len, 128) splits per head).
+// and max_splits (part[] must hold cdiv(max_seq_len, kAttnMinSplit) splits per
+// head).
+constexpr int kAttnMinSplit = 128;   // 64 measured slower (profiles/r1/optimisation_log.md)
 void plan_decode_attn(DecodeAttnParams& p, const int* ctx_host);
 
 // Prefill: varlen causal over each sequence's own (paged) K/V.

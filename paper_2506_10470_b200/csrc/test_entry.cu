@@ -170,7 +170,7 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
   for (int c = 0; c < copies; ++c)
     for (int i = 0; i < n; ++i)
       for (int b = 0; b < (ctx[i] + 15) / 16; ++b) bt[((size_t)c * n + i) * maxblk + b] = perm[k++];
-  const int cap = (max_ctx + 127) / 128;
+  const int cap = (max_ctx + kAttnMinSplit - 1) / kAttnMinSplit;
   bf16 *kv = nullptr, *q = nullptr, *o = nullptr;
   float* part = nullptr;
   int32_t *dctx = nullptr, *dbt = nullptr;
