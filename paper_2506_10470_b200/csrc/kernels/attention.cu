@@ -158,6 +158,9 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
   constexpr bool PF = G <= 2;
   uint4 kr[U], vr[U], kn[U], vn[U];
   bool valid[U], vnx[U];
+  // K/V are read once per layer: evict-first, so they do not push
+  // activations, split-K partials or metadata out of L2
+  const uint64_t kvpol = l2_evict_first_policy();
   auto issue = [&](int base, uint4* K, uint4* Vv, bool* ok) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -166,8 +169,8 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
       const int tt = ok[u] ? t : t_begin;
       const int blk = bt[tt >> 4];
       const int64_t kb = (((int64_t)blk * 2) * p.Hkv + kh) * head_stride + (tt & 15) * HD + sub * 8;
-      K[u] = ld_nc_v4(p.kv + kb);
-      Vv[u] = ld_nc_v4(p.kv + kb + (int64_t)p.Hkv * head_stride);
+      K[u] = ld_nc_v4_ef(p.kv + kb, kvpol);
+      Vv[u] = ld_nc_v4_ef(p.kv + kb + (int64_t)p.Hkv * head_stride, kvpol);
     }
   };
   // The first step's K/V loads go out before the PDL wait: every context

@@ -45,6 +45,19 @@ TDP_DEV uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
+// streaming read that is not kept in L2 (evict-first cache policy `pol`)
+TDP_DEV uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+TDP_DEV uint4 ld_nc_v4_ef(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+
 TDP_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 TDP_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
