@@ -246,13 +246,14 @@ decode_attn_kernel(DecodeAttnParams p) {
   // previous kernel ran): read before the PDL wait, which attend_range takes
   const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
   const int ctx = p.ctx[seq];
-  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
+  const int len = p.split_tokens;
+  const int n_splits = (ctx + len - 1) / len;
   if (split >= n_splits) {
     pdl_wait();
     return;
   }
-  const int t_begin = split * p.split_tokens;
-  attend_range<HD, G>(p, seq, kh, t_begin, min(ctx, t_begin + p.split_tokens), split, n_splits, ctx - 1);
+  const int t_begin = split * len;
+  attend_range<HD, G>(p, seq, kh, t_begin, min(ctx, t_begin + len), split, n_splits, ctx - 1);
 }
 
 // ---------------------------------------------------------------- decode v2
