@@ -40,10 +40,14 @@ typedef int32_t td_status;
 
 /* Scheduling policies.  TDPIPE = the paper's method (§3.3-§3.5); PPSB_* are the
  * naive phase-interleaved PP + separate-batching baselines:
- * PRIO issues a prefill whenever one is admissible, ALT alternates. */
+ * PRIO issues a prefill whenever one is admissible, ALT alternates.  PPHB =
+ * PP + hybrid batching with chunked prefill:
+ * every micro-batch carries its engine's decode tokens plus prefill chunks up
+ * to hb_tokens (reading R23). */
 #define TD_POLICY_TDPIPE 0
 #define TD_POLICY_PPSB_PRIO 1
 #define TD_POLICY_PPSB_ALT 2
+#define TD_POLICY_PPHB 3
 
 /* Executors.  CUDA = the real sm_100a path.  NULL = controller only (no GPU
  * touched; micro-batches complete logically) -- used to test the scheduler. */
@@ -89,6 +93,7 @@ typedef struct td_options {
   /* ablations of the paper's §4.4 (0 = the paper's method) */
   int32_t p2d_kv_permille;      /* P->D once allocated KV >= x/1000 of C */
   int32_t d2p_finish_permille;  /* D->P once x/1000 of the decode cohort finished */
+  int32_t hb_tokens;            /* PPHB: tokens per hybrid micro-batch (default 512)   */
 } td_options;
 
 typedef struct td_run_stats {

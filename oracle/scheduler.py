@@ -11,7 +11,9 @@ The TD-Pipe control plane, step by step in the paper's order and notation:
   temporal intensity" (§3.5),
 * recompute on KV overflow, "KV cache of recently arrived requests will be
   freed" (§4.1),
-* the naive PP+SB baselines (PAPER.md:108 fig:pipeline_bubble; 530 §4.1).
+* the naive PP+SB baselines (PAPER.md:108 fig:pipeline_bubble; 530 §4.1),
+* the PP+HB baseline: hybrid batching with chunked prefill (PAPER.md:125-128
+  §1, 255-260 §2.3, 531 §4.1) [R23].
 
 Logical time only: the only external events are micro-batch returns, which
 arrive in launch order because every stage is FIFO, so
@@ -32,7 +34,7 @@ from typing import List, Optional
 
 import numpy as np
 
-TDPIPE, PPSB_PRIO, PPSB_ALT = 0, 1, 2
+TDPIPE, PPSB_PRIO, PPSB_ALT, PPHB = 0, 1, 2, 3
 
 
 def ceil_div(a: int, b: int) -> int:
@@ -55,6 +57,7 @@ class SchedOptions:
     # ablations (§4.4.1, 660-662 §4.4.3); 0 = the paper's method
     p2d_kv_permille: int = 0            # switch to decode once allocated KV >= ratio * C
     d2p_finish_permille: int = 0        # switch to prefill once this fraction of the decode cohort finished
+    hb_tokens: int = 512                # PP+HB: tokens per hybrid micro-batch (decode tokens + prefill chunks) [R23]
 
 
 @dataclass
@@ -72,12 +75,13 @@ class Req:
     in_flight: bool = False
     done: bool = False
     slot: int = -1  # current-formation slot or -1 (pool / none)
+    pf: int = 0     # PP+HB: prompt tokens prefilled so far (chunked prefill)
 
 
 @dataclass
 class MicroBatch:
     mid: int
-    kind: str                 # 'P' or 'D'
+    kind: str                 # 'P', 'D' or 'H' (hybrid: decode members first, then prefill chunks)
     members: List[int]
     q_start: List[int]
     q_len: List[int]
@@ -567,6 +571,8 @@ class RefScheduler:
     # ------------------------------------------------------------ main loop
     def run(self):
         self._evict_key = {}
+        if self.o.policy == PPHB:
+            return self._run_hybrid()
         if self.o.policy != TDPIPE:
             return self._run_baseline()
         if not self.reqs:
@@ -699,6 +705,161 @@ class RefScheduler:
                     running[e].remove(rid)
             issue(e)
         assert all(r.done for r in self.reqs), "baseline stalled"
+        return self
+
+
+    # ------------------------------------------------------------ PP+HB
+    def _run_hybrid(self):
+        """PP+HB baseline [R23]: "hybrid batching combines requests from both
+        the prefill and decode phases into the same batch" with "chunked
+        prefill [that] splits the prefill into chunks".
+        As the PP+SB baselines: W virtual engines (one micro-batch in flight
+        each), request r on engine r mod W, per-engine KV quota C/W.  Each
+        micro-batch of engine e = all its decoding requests (one token each,
+        admission order) + prefill chunks filling the rest of hb_tokens: first
+        the engine's partially prefilled requests, then its pending ones
+        (evicted first, then fresh).  A chunk takes min(remaining prompt,
+        token budget left, tokens whose blocks fit the quota); the chunk that
+        completes a prompt produces the first token and the request decodes
+        from the next micro-batch on.  KV overflow of the decode step evicts
+        (recompute) the most recently admitted running or prefilling request."""
+        W = self.W
+        T = max(self.o.hb_tokens, 1)
+        quota = [self.C // W + (1 if e < self.C % W else 0) for e in range(W)]
+        used = [0] * W
+        q_ev = [[] for _ in range(W)]
+        q_fr = [deque() for _ in range(W)]
+        for r in self.reqs:
+            q_fr[r.rid % W].append(r.rid)
+        running = [[] for _ in range(W)]    # decoding, admission order
+        filling = [[] for _ in range(W)]    # 0 < pf < L, admission order
+        ekey = {}
+        for r in self.reqs:
+            if ceil_div(r.L + r.N, self.B) > quota[r.rid % W]:
+                raise ValueError("request exceeds its engine's KV quota")
+
+        def evict(e, victim):
+            r = self.reqs[victim]
+            used[e] -= len(r.blocks)
+            old = r.adm
+            self.alloc.release(r.blocks)
+            self.emit("E", victim, *r.blocks)
+            r.blocks = []
+            if victim in running[e]:
+                running[e].remove(victim)
+            else:
+                filling[e].remove(victim)
+            r.L += r.g
+            r.N -= r.g
+            r.P = max(r.P - r.g, 1)
+            r.g = r.d = r.pf = 0
+            r.adm = -1
+            self.live.discard(victim)
+            ekey[victim] = old
+            pos = 0
+            while pos < len(q_ev[e]) and ekey[q_ev[e][pos]] < old:
+                pos += 1
+            q_ev[e].insert(pos, victim)
+            self.stats["evicted"] += 1
+
+        def plan(e):
+            dec = list(running[e])
+            avail = quota[e] - used[e] - self.decode_need(dec)
+            budget = T - len(dec)
+            chunks = []          # (rid, q_start, q_len)
+            for rid in list(filling[e]) + list(q_ev[e]) + list(q_fr[e]):
+                if budget <= 0:
+                    break
+                r = self.reqs[rid]
+                fit = (len(r.blocks) + avail) * self.B - r.pf     # tokens whose blocks fit the quota
+                take = min(r.L - r.pf, budget, fit)
+                if take <= 0:
+                    break
+                avail -= ceil_div(r.pf + take, self.B) - len(r.blocks)
+                chunks.append((rid, r.pf, take))
+                budget -= take
+            return dec, chunks
+
+        def issue(e):
+            # decode step of the running requests; evict while it does not fit
+            while running[e] and self.decode_need(running[e]) > quota[e] - used[e]:
+                evict(e, max(running[e] + filling[e], key=lambda i: self.reqs[i].adm))
+            dec, chunks = plan(e)
+            # partially prefilled prompts alone can exhaust the quota: recompute
+            # the most recently admitted one until something fits
+            while not dec and not chunks and filling[e]:
+                evict(e, max(filling[e], key=lambda i: self.reqs[i].adm))
+                dec, chunks = plan(e)
+            if not dec and not chunks:
+                return           # engine idle
+            for rid in dec:
+                r = self.reqs[rid]
+                k = ceil_div(r.L + r.d + 1, self.B) - len(r.blocks)
+                if k > 0:
+                    blk = self.alloc.alloc(k)
+                    r.blocks.extend(blk)
+                    used[e] += k
+                    self.emit("A", rid, *blk)
+            for rid, q0, ql in chunks:
+                r = self.reqs[rid]
+                if r.pf == 0 and rid not in filling[e]:     # admission
+                    if q_ev[e] and q_ev[e][0] == rid:
+                        q_ev[e].pop(0)
+                    else:
+                        q_fr[e].popleft()
+                    r.adm = self.adm_counter
+                    self.adm_counter += 1
+                    r.g = r.d = 0
+                    self.live.add(rid)
+                    filling[e].append(rid)
+                k = ceil_div(q0 + ql, self.B) - len(r.blocks)
+                if k > 0:
+                    blk = self.alloc.alloc(k)
+                    r.blocks.extend(blk)
+                    used[e] += k
+                    self.emit("A", rid, *blk)
+            mid = self.mb_counter
+            self.mb_counter += 1
+            mem = dec + [c[0] for c in chunks]
+            mb = MicroBatch(mid, "H", mem, [self.reqs[i].L + self.reqs[i].d for i in dec] + [c[1] for c in chunks],
+                            [1] * len(dec) + [c[2] for c in chunks], e, 0)
+            for rid in mem:
+                self.reqs[rid].in_flight = True
+            self.inflight.append(mb)
+            self.plan.append(mb)
+            self.emit("H", mid, e, len(dec), len(chunks), *dec, *["%d:%d:%d" % c for c in chunks])
+
+        for e in range(W):
+            issue(e)
+        while self.inflight:
+            mb = self.inflight.popleft()
+            e = mb.slot
+            self.emit("R", mb.mid, len(mb.members), *mb.members)
+            for rid, q0, ql in zip(mb.members, mb.q_start, mb.q_len):
+                r = self.reqs[rid]
+                r.in_flight = False
+                if rid in running[e]:           # decode token
+                    r.g += 1
+                    r.n_out += 1
+                    r.d += 1
+                else:                           # prefill chunk
+                    r.pf = q0 + ql
+                    if r.pf < r.L:
+                        continue
+                    filling[e].remove(rid)      # prompt complete: first token
+                    running[e].append(rid)
+                    r.g += 1
+                    r.n_out += 1
+                if r.g == r.N:
+                    used[e] -= len(r.blocks)
+                    r.done = True
+                    self.alloc.release(r.blocks)
+                    self.emit("F", rid, *r.blocks)
+                    r.blocks = []
+                    self.live.discard(rid)
+                    running[e].remove(rid)
+            issue(e)
+        assert all(r.done for r in self.reqs), "hybrid baseline stalled"
         return self
 
 

@@ -70,6 +70,7 @@ extern "C" void td_default_options(td_options* o) {
   o->nccl_ids = nullptr;
   o->p2d_kv_permille = 0;
   o->d2p_finish_permille = 0;
+  o->hb_tokens = 512;
 }
 
 static bool read_profile(const std::string& path, std::vector<int64_t>* tdec, std::vector<int64_t>* tpre,
@@ -184,6 +185,7 @@ extern "C" td_status td_run(td_ctx* c, td_run_stats* st) {
   so.eq2_bubble_scale = c->opt.eq2_bubble_scale;
   so.p2d_kv_permille = c->opt.p2d_kv_permille;
   so.d2p_finish_permille = c->opt.d2p_finish_permille;
+  so.hb_tokens = c->opt.hb_tokens;
   if (so.policy == TD_POLICY_TDPIPE && c->tdec.size() < 2 && c->reqs.size() > 0) {
     // without a profile table Eq.1/Eq.2 cannot be evaluated: use a flat one
     // (never switches before the queue drains is NOT implied; document it)
@@ -263,7 +265,19 @@ struct SimHooks : ExecHooks {
   int launch(const MicroBatch& mb, const std::vector<Req>& reqs) override {
     int64_t tok = 0;
     for (int q : mb.q_len) tok += q;
-    const int64_t t = mb.kind == 'P' ? at(tpre, tok) : at(tdec, (int64_t)mb.members.size());
+    int64_t t;
+    if (mb.kind == 'H') {
+      // hybrid micro-batch [R23]: the GEMMs see all its tokens like a prefill
+      // of that many tokens (and stream the weights at least once, D(1)); the
+      // decode members add their attention, taken as the decode table's growth
+      // over a batch of one.  The chunks' re-read of their prefix KV is not
+      // charged (favours PP+HB)
+      int64_t nd = 0;
+      for (size_t i = 0; i < mb.members.size(); ++i) nd += mb.q_start[i] >= reqs[mb.members[i]].L ? 1 : 0;
+      t = std::max(at(tpre, tok), at(tdec, 1)) + (nd > 0 ? std::max<int64_t>(0, at(tdec, nd) - at(tdec, 1)) : 0);
+    } else {
+      t = mb.kind == 'P' ? at(tpre, tok) : at(tdec, (int64_t)mb.members.size());
+    }
     int64_t arrive = now;
     for (int s = 0; s < S; ++s) {
       const int64_t start = std::max(arrive, free_at[s]);
@@ -305,6 +319,7 @@ extern "C" td_status td_simulate(td_ctx* c, td_run_stats* st, int64_t host_retur
   so.eq2_bubble_scale = c->opt.eq2_bubble_scale;
   so.p2d_kv_permille = c->opt.p2d_kv_permille;
   so.d2p_finish_permille = c->opt.d2p_finish_permille;
+  so.hb_tokens = c->opt.hb_tokens;
   std::vector<Req> reqs(c->reqs.size());
   for (size_t i = 0; i < c->reqs.size(); ++i) {
     reqs[i].rid = (int)i;

@@ -650,8 +650,194 @@ int Controller::run_baseline() {
   return 0;
 }
 
+// ------------------------------------------------------------ PP+HB [R23]
+// Hybrid batching with chunked prefill: the
+// PP+SB engine layout (W virtual engines, r mod W, quota C/W); each micro-batch
+// = the engine's decoding requests (one token each, admission order) + prefill
+// chunks up to hb_tokens (partially prefilled prompts first, then pending
+// ones, evicted before fresh); a chunk is min(remaining prompt, budget left,
+// tokens whose blocks fit).  The chunk completing a prompt yields the first
+// token.  Mirrors oracle/scheduler.py RefScheduler._run_hybrid line by line.
+int Controller::run_hybrid() {
+  const int W = opt_.W;
+  const int T = std::max(opt_.hb_tokens, 1);
+  std::vector<int64_t> quota(W), used(W, 0);
+  for (int e = 0; e < W; ++e) quota[e] = opt_.C / W + (e < opt_.C % W ? 1 : 0);
+  std::vector<std::vector<int>> q_ev(W), running(W), filling(W);
+  std::vector<std::deque<int>> q_fr(W);
+  for (auto& r : reqs_) q_fr[r.rid % W].push_back(r.rid);
+  for (auto& r : reqs_)
+    if (ceil_div((int64_t)r.L + r.N, opt_.B) > quota[r.rid % W]) {
+      error = "request exceeds its engine's KV quota";
+      return -5;
+    }
+  auto contains = [](const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); };
+  auto max_adm = [&](const std::vector<int>& v) {
+    int victim = -1;
+    int64_t best = -2;
+    for (int rid : v) if (reqs_[rid].adm > best) { best = reqs_[rid].adm; victim = rid; }
+    return victim;
+  };
+  auto evict = [&](int e, int victim) {
+    Req& r = reqs_[victim];
+    used[e] -= (int64_t)r.blocks.size();
+    const int64_t old = r.adm;
+    release(r.blocks);
+    std::vector<int64_t> line{victim};
+    for (int32_t b : r.blocks) line.push_back(b);
+    emit_ids("E", line);
+    r.blocks.clear();
+    auto& from = contains(running[e], victim) ? running[e] : filling[e];
+    from.erase(std::find(from.begin(), from.end(), victim));
+    r.L += r.g;
+    r.N -= r.g;
+    r.P = std::max(r.P - r.g, 1);
+    r.g = r.d = r.pf = 0;
+    r.adm = -1;
+    live_.erase(victim);
+    size_t pos = 0;
+    while (pos < q_ev[e].size() && reqs_[q_ev[e][pos]].evict_key < old) ++pos;
+    r.evict_key = old;
+    q_ev[e].insert(q_ev[e].begin() + pos, victim);
+    stats_.evicted++;
+  };
+  struct Chunk { int rid, q0, ql; };
+  auto plan = [&](int e, std::vector<int>& dec, std::vector<Chunk>& chunks) {
+    dec = running[e];
+    chunks.clear();
+    int64_t avail = quota[e] - used[e] - decode_need(dec);
+    int64_t budget = T - (int64_t)dec.size();
+    std::vector<int> cands(filling[e]);
+    cands.insert(cands.end(), q_ev[e].begin(), q_ev[e].end());
+    cands.insert(cands.end(), q_fr[e].begin(), q_fr[e].end());
+    for (int rid : cands) {
+      if (budget <= 0) break;
+      const Req& r = reqs_[rid];
+      const int64_t fit = ((int64_t)r.blocks.size() + avail) * opt_.B - r.pf;
+      const int64_t take = std::min<int64_t>({(int64_t)r.L - r.pf, budget, fit});
+      if (take <= 0) break;
+      avail -= ceil_div((int64_t)r.pf + take, opt_.B) - (int64_t)r.blocks.size();
+      chunks.push_back({rid, r.pf, (int)take});
+      budget -= take;
+    }
+  };
+  auto issue = [&](int e) -> int {
+    while (!running[e].empty() && decode_need(running[e]) > quota[e] - used[e]) {
+      std::vector<int> cands(running[e]);
+      cands.insert(cands.end(), filling[e].begin(), filling[e].end());
+      evict(e, max_adm(cands));
+    }
+    std::vector<int> dec;
+    std::vector<Chunk> chunks;
+    plan(e, dec, chunks);
+    while (dec.empty() && chunks.empty() && !filling[e].empty()) {
+      evict(e, max_adm(filling[e]));
+      plan(e, dec, chunks);
+    }
+    if (dec.empty() && chunks.empty()) return 0;   // engine idle
+    auto grow = [&](int rid, int64_t tokens) {
+      Req& r = reqs_[rid];
+      const int64_t k = ceil_div(tokens, opt_.B) - (int64_t)r.blocks.size();
+      if (k > 0) {
+        std::vector<int64_t> line{rid};
+        for (int64_t i = 0; i < k; ++i) { int32_t b = alloc_one(); r.blocks.push_back(b); line.push_back(b); }
+        used[e] += k;
+        emit_ids("A", line);
+      }
+    };
+    for (int rid : dec) grow(rid, (int64_t)reqs_[rid].L + reqs_[rid].d + 1);
+    for (const Chunk& c : chunks) {
+      Req& r = reqs_[c.rid];
+      if (r.pf == 0 && !contains(filling[e], c.rid)) {   // admission
+        if (!q_ev[e].empty() && q_ev[e].front() == c.rid) q_ev[e].erase(q_ev[e].begin());
+        else q_fr[e].pop_front();
+        r.adm = adm_counter_++;
+        r.g = r.d = 0;
+        live_.insert(c.rid);
+        filling[e].push_back(c.rid);
+      }
+      grow(c.rid, (int64_t)c.q0 + c.ql);
+    }
+    MicroBatch mb;
+    mb.mid = mb_counter_++;
+    mb.kind = 'H';
+    mb.slot = e;
+    mb.epoch = 0;
+    for (int rid : dec) {
+      mb.members.push_back(rid);
+      mb.q_start.push_back(reqs_[rid].L + reqs_[rid].d);
+      mb.q_len.push_back(1);
+    }
+    for (const Chunk& c : chunks) {
+      mb.members.push_back(c.rid);
+      mb.q_start.push_back(c.q0);
+      mb.q_len.push_back(c.ql);
+    }
+    for (int rid : mb.members) reqs_[rid].in_flight = true;
+    if (keep_log_) {
+      std::string line = "H " + std::to_string(mb.mid) + " " + std::to_string(e) + " " + std::to_string(dec.size()) +
+                         " " + std::to_string(chunks.size());
+      for (int rid : dec) line += " " + std::to_string(rid);
+      for (const Chunk& c : chunks)
+        line += " " + std::to_string(c.rid) + ":" + std::to_string(c.q0) + ":" + std::to_string(c.ql);
+      emit(line);
+    }
+    stats_.n_mb++;
+    if (dec.empty()) stats_.n_prefill++;
+    else stats_.n_decode++;
+    for (const Chunk& c : chunks) stats_.prompt_tokens += c.ql;
+    inflight_.push_back(mb);
+    return ex_ ? ex_->launch(inflight_.back(), reqs_) : 0;
+  };
+
+  for (int e = 0; e < W; ++e) if (int rc = issue(e)) return rc;
+  while (!inflight_.empty()) {
+    MicroBatch mb = std::move(inflight_.front());
+    inflight_.pop_front();
+    const int e = mb.slot;
+    {
+      std::vector<int64_t> line{mb.mid, (int64_t)mb.members.size()};
+      for (int rid : mb.members) line.push_back(rid);
+      emit_ids("R", line);
+    }
+    if (ex_) if (int rc = ex_->returned(mb)) return rc;
+    for (size_t i = 0; i < mb.members.size(); ++i) {
+      const int rid = mb.members[i];
+      Req& r = reqs_[rid];
+      r.in_flight = false;
+      if (contains(running[e], rid)) {        // decode token
+        r.g++;
+        r.n_out++;
+        r.d++;
+      } else {                                // prefill chunk
+        r.pf = mb.q_start[i] + mb.q_len[i];
+        if (r.pf < r.L) continue;
+        filling[e].erase(std::find(filling[e].begin(), filling[e].end(), rid));
+        running[e].push_back(rid);            // prompt complete: first token
+        r.g++;
+        r.n_out++;
+      }
+      if (r.g == r.N) {
+        used[e] -= (int64_t)r.blocks.size();
+        r.done = true;
+        release(r.blocks);
+        std::vector<int64_t> line{rid};
+        for (int32_t b : r.blocks) line.push_back(b);
+        emit_ids("F", line);
+        r.blocks.clear();
+        live_.erase(rid);
+        running[e].erase(std::find(running[e].begin(), running[e].end(), rid));
+      }
+    }
+    if (int rc = issue(e)) return rc;
+  }
+  for (auto& r : reqs_) if (!r.done) { error = "hybrid baseline stalled"; return -6; }
+  return 0;
+}
+
 int Controller::run(ExecHooks* ex) {
   ex_ = ex;
+  if (opt_.policy == kPPHB) return run_hybrid();
   return opt_.policy == kTDPipe ? run_tdpipe() : run_baseline();
 }
 

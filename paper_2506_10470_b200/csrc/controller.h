@@ -13,7 +13,8 @@
 //   S6     return processing; S7 work stealing
 //   S8     recompute eviction
 //   S9/S10 Eq.1 / Eq.2 and the switch rule
-//   S11    naive PP+SB baselines; S12 decision log
+//   S11    naive PP+SB baselines; PP+HB hybrid batching + chunked prefill [R23];
+//          S12 decision log
 #pragma once
 #include <cstdint>
 #include <deque>
@@ -24,7 +25,7 @@
 
 namespace tdp {
 
-enum Policy { kTDPipe = 0, kPPSBPrio = 1, kPPSBAlt = 2 };
+enum Policy { kTDPipe = 0, kPPSBPrio = 1, kPPSBAlt = 2, kPPHB = 3 };
 
 struct SchedOptions {
   int W = 1;                 // pipeline stages = decode batches
@@ -40,6 +41,7 @@ struct SchedOptions {
   int eq2_bubble_scale = 1;
   int p2d_kv_permille = 0;      // ablation A22: KV-occupancy-ratio P->D switch
   int d2p_finish_permille = 0;  // ablation A23: request-finish-ratio D->P switch
+  int hb_tokens = 512;          // PP+HB: tokens per hybrid micro-batch [R23]
 };
 
 struct Req {
@@ -57,11 +59,12 @@ struct Req {
   bool done = false;
   int slot = -1;
   int64_t evict_key = -1;
+  int pf = 0;     // PP+HB: prompt tokens prefilled so far
 };
 
 struct MicroBatch {
   int64_t mid = 0;
-  char kind = 'P';
+  char kind = 'P';   // 'P', 'D' or 'H' (PP+HB: decode members first, then prefill chunks)
   int slot = -1;
   int epoch = 0;
   std::vector<int> members, q_start, q_len;
@@ -131,6 +134,7 @@ class Controller {
   int on_return(const MicroBatch& mb);
   int run_tdpipe();
   int run_baseline();
+  int run_hybrid();
   // allocator (lowest free id first)
   int64_t free_blocks() const { return opt_.C - watermark_ + (int64_t)free_heap_.size(); }
   int32_t alloc_one();

@@ -60,8 +60,11 @@ struct XOps {
 // Per-micro-batch metadata (host-built, one H2D copy): int32 arrays.
 struct Meta {
   int n = 0, T = 0, maxblk = 0, max_ctx = 0, prefill = 0;
+  // PP+HB hybrid micro-batch: members [0, nd) decode one token, members
+  // [nd, n) are prefill chunks (q_start >= 0) of at most max_qlen tokens
+  int hybrid = 0, nd = 0, max_qlen = 0;
   // offsets (in int32 units) into the packed buffer
-  int o_ctx, o_tokidx, o_pos, o_slot, o_seq, o_last, o_outpos, o_bt;
+  int o_ctx, o_tokidx, o_pos, o_slot, o_seq, o_last, o_outpos, o_bt, o_qs;
   int total = 0;
 };
 
@@ -103,6 +106,7 @@ class CudaEngine : public Engine {
   td_status ensure_work(int64_t T, int64_t n, int64_t maxblk);
   // build metadata into ring slot `r`; returns the packed layout
   Meta build_meta(int r, bool prefill, int n, const int* q_start, const int* q_len, const int32_t* arena_off,
+                  const char* emit,
                   const std::vector<const std::vector<int32_t>*>& blocks, const int32_t* bt_flat, int bt_stride);
   td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena);
   td_status run_microbatch(const Meta& M, const int32_t* dmeta, int32_t* arena);
@@ -505,7 +509,7 @@ int CudaEngine::ring_acquire() {
 }
 
 Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, const int* q_len,
-                            const int32_t* arena_off, const std::vector<const std::vector<int32_t>*>& blocks,
+                            const int32_t* arena_off, const char* emit, const std::vector<const std::vector<int32_t>*>& blocks,
                             const int32_t* bt_flat, int bt_stride) {
   Meta M;
   M.n = n;
@@ -529,6 +533,7 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
   M.o_slot = off; off += T;
   M.o_seq = off; off += T;
   M.o_bt = off; off += n * maxblk;
+  M.o_qs = off; off += n;
   M.total = off;
   int32_t* h = hmeta_[r];
   int t = 0;
@@ -549,7 +554,9 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
       h[M.o_seq + t] = i;
     }
     h[M.o_last + i] = t - 1;
-    h[M.o_outpos + i] = arena_off ? arena_off[i] + ctx : 0;
+    // no token for a prefill chunk that does not complete its prompt (PP+HB)
+    h[M.o_outpos + i] = emit && !emit[i] ? -1 : arena_off ? arena_off[i] + ctx : 0;
+    h[M.o_qs + i] = q_start[i];
   }
   return M;
 }
@@ -622,9 +629,28 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     if (iq >= 0 && !M.prefill) timed_[iq].sub = kGemmBucket + bucket_of(T);
     gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
-    if (M.prefill) {
+    if (M.hybrid) {
+      // PP+HB: decode members [0, nd) -- one token each, so token row = member
+      // index, as the decode kernel expects -- and prefill chunks [nd, n)
+      // attending to their paged prefix + causal chunk
+      if (M.nd > 0) {
+        DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, M.nd, H_, Hkv_, hd_, 0,
+                            attn_cnt_};
+        plan_decode_attn(dp, mb_ctx_.data());
+        launch_decode_attn(dp, st_);
+        launches_++;
+      }
+      if (M.nd < n) {
+        const int nc = n - M.nd;
+        PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt + (int64_t)M.nd * M.maxblk, M.maxblk,
+                             ob_, T, H_, Hkv_, hd_, dm + M.o_ctx + M.nd, dm + M.o_last + M.nd, nc, M.max_qlen,
+                             dm + M.o_qs + M.nd};
+        launch_prefill_attn(pp, st_);
+        launches_++;
+      }
+    } else if (M.prefill) {
       PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_,
-                           dm + M.o_ctx, dm + M.o_last, n, M.max_ctx};
+                           dm + M.o_ctx, dm + M.o_last, n, M.max_ctx, nullptr};
       const int ip = tbegin(cPreAttn);
       launch_prefill_attn(pp, st_);
       tend(ip, 0, 0);
@@ -828,7 +854,24 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
     }
   }
   const int r = ring_acquire();
-  Meta M = build_meta(r, mb.kind == 'P', n, mb.q_start.data(), mb.q_len.data(), aoff.data(), blocks, nullptr, 0);
+  // PP+HB hybrid micro-batch: decode members (q_start >= L) lead, then chunks;
+  // a chunk emits a token only if it completes its prompt
+  std::vector<char> emit(n, 1);
+  int nd = 0;
+  if (mb.kind == 'H') {
+    for (int i = 0; i < n; ++i) {
+      const Req& rq = reqs[mb.members[i]];
+      emit[i] = mb.q_start[i] + mb.q_len[i] >= rq.L;
+      if (mb.q_start[i] >= rq.L && i == nd) ++nd;
+    }
+  }
+  Meta M = build_meta(r, mb.kind == 'P', n, mb.q_start.data(), mb.q_len.data(), aoff.data(), emit.data(), blocks,
+                      nullptr, 0);
+  if (mb.kind == 'H') {
+    M.hybrid = 1;
+    M.nd = nd;
+    for (int i = nd; i < n; ++i) M.max_qlen = std::max(M.max_qlen, mb.q_len[i]);
+  }
   if (cudaMemcpyAsync(dmeta_[r], hmeta_[r], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_) != cudaSuccess) {
     error = "metadata H2D failed";
     return TD_ECUDA;
@@ -866,6 +909,7 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
     cudaMemcpyAsync(hlogits_, logits_, (size_t)n * V_ * 4, cudaMemcpyDeviceToHost, st_);
     if (cudaStreamSynchronize(st_) != cudaSuccess) { error = "sync failed"; return TD_ECUDA; }
     for (int i = 0; i < n; ++i) {
+      if (!emit[i]) continue;
       auto& v = rec_[mb.members[i]];
       v.insert(v.end(), hlogits_ + (size_t)i * V_, hlogits_ + (size_t)(i + 1) * V_);
     }
@@ -961,7 +1005,8 @@ td_status CudaEngine::stage_forward(int stage, const td_batch& b, const void* in
   CK(cudaStreamSynchronize(st_));
   for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
   const int r = 0;
-  Meta M = build_meta(r, b.kind == TD_BATCH_PREFILL, n, b.q_start, b.q_len, nullptr, {}, b.block_table, b.max_blocks);
+  Meta M = build_meta(r, b.kind == TD_BATCH_PREFILL, n, b.q_start, b.q_len, nullptr, nullptr, {}, b.block_table,
+                      b.max_blocks);
   CK(cudaMemcpyAsync(dmeta_[r], hmeta_[r], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_));
   int32_t* tok = nullptr;
   if (stage == 0) {
@@ -1003,7 +1048,7 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
     for (int i = 0; i < n; ++i)
       for (int k = 0; k <= nb; ++k) bt[(size_t)i * (nb + 1) + k] = (int32_t)(((int64_t)i * (nb + 1) + k) % C_);
     for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
-    Meta M = build_meta(0, prefill, n, qs.data(), ql.data(), nullptr, {}, bt.data(), nb + 1);
+    Meta M = build_meta(0, prefill, n, qs.data(), ql.data(), nullptr, nullptr, {}, bt.data(), nb + 1);
     CK(cudaMemcpyAsync(dmeta_[0], hmeta_[0], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_));
     int64_t worst = 0;
     for (int s = own_s0_; s < own_s1_; ++s) {

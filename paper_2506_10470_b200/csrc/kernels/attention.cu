@@ -590,10 +590,12 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
   pdl_trigger();
   pdl_wait();
   const int qt = blockIdx.x, seq = blockIdx.y, h = blockIdx.z;
-  const int L = p.seq_ctx[seq];
-  const int q0 = qt * BQ;
-  if (q0 >= L) return;
-  const int row0 = p.seq_last[seq] - L + 1;     // first token row of this sequence
+  const int L = p.seq_ctx[seq];                  // keys: positions 0 .. L-1
+  const int qs = p.seq_qstart ? p.seq_qstart[seq] : 0;
+  const int nq = L - qs;                         // queries: positions qs .. L-1
+  const int q0 = qt * BQ;                        // (query indices relative to qs)
+  if (q0 >= nq) return;
+  const int row0 = p.seq_last[seq] - nq + 1;    // token row of query 0
   const int G = p.H / p.Hkv, kh = h / G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
@@ -603,8 +605,8 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
   for (int i = tid; i < BQ * CH; i += 128) {
     const int r = i / CH, c = i % CH;
     const int q = q0 + r;
-    const bf16* src = p.q + ((int64_t)(row0 + (q < L ? q : 0)) * p.H + h) * HD + c * 8;
-    cp_async16(sQ + fswz<HD>(r, c) * 16, src, q < L);
+    const bf16* src = p.q + ((int64_t)(row0 + (q < nq ? q : 0)) * p.H + h) * HD + c * 8;
+    cp_async16(sQ + fswz<HD>(r, c) * 16, src, q < nq);
   }
   auto load_kv = [&](int stage, int k0) {
     for (int i = tid; i < BKV * CH; i += 128) {
@@ -617,7 +619,7 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
       cp_async16(sV + stage * TILE + fswz<HD>(r, c) * 16, p.kv + base + (int64_t)p.Hkv * head_stride, ok);
     }
   };
-  const int last_q = min(q0 + BQ, L) - 1;
+  const int last_q = qs + min(q0 + BQ, nq) - 1;   // absolute position of the tile's last query
   const int n_kt = last_q / BKV + 1;
   load_kv(0, 0);
   cp_async_commit();
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
   float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
   uint32_t qf[HD / 16][4];
   const int g = lane >> 2, tq = lane & 3;
-  const int qr0 = q0 + warp * 16 + g;     // this thread's two query positions: qr0, qr0 + 8
+  const int qr0 = q0 + warp * 16 + g;     // this thread's two queries (relative): qr0, qr0 + 8
 
   for (int kt = 0; kt < n_kt; ++kt) {
     if (kt + 1 < n_kt) load_kv((kt + 1) & 1, (kt + 1) * BKV);
@@ -665,7 +667,7 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int key = k0 + ni * 8 + 2 * tq + (e & 1);
-        const int qp = qr0 + (e >> 1) * 8;
+        const int qp = qs + qr0 + (e >> 1) * 8;   // absolute query position (causal bound)
         const float v = (key <= qp && key < L) ? s[ni][e] * sl2 : -INFINITY;
         s[ni][e] = v;
         mx[e >> 1] = fmaxf(mx[e >> 1], v);
@@ -725,7 +727,7 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int q = qr0 + rr * 8;
-    if (q >= L) continue;
+    if (q >= nq) continue;
     const float inv = 1.f / l_r[rr];
     bf16* dst = p.o + ((int64_t)(row0 + q) * p.H + h) * HD;
 #pragma unroll

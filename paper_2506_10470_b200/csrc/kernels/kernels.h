@@ -99,9 +99,10 @@ struct PrefillAttnParams {
   int maxblk;
   bf16* o;                  // [T, H*hd]
   int T, H, Hkv, hd;
-  const int32_t* seq_ctx;   // [n] sequence length (prefill: q_start = 0)
+  const int32_t* seq_ctx;   // [n] context length after this step (= q_start + q_len)
   const int32_t* seq_last;  // [n] row of the sequence's last token
-  int n_seqs, max_len;
+  int n_seqs, max_len;      // max_len >= every q_len
+  const int32_t* seq_qstart;  // [n] first query position (chunked prefill); nullptr = all 0
 };
 void launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t st);
 

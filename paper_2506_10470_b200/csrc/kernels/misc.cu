@@ -344,7 +344,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* 
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    if (threadIdx.x == 0) arena[outpos[i]] = bi;
+    if (threadIdx.x == 0 && outpos[i] >= 0) arena[outpos[i]] = bi;   // -1: no token (PP+HB chunk)
   }
 }
 
@@ -362,13 +362,13 @@ __global__ void token_pairs_kernel(const int32_t* __restrict__ arena, const int3
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int p = outpos[i];
     pairs[2 * i] = p;
-    pairs[2 * i + 1] = arena[p];
+    pairs[2 * i + 1] = p >= 0 ? arena[p] : 0;
   }
 }
 // stage 0: scatter received pairs into its token arena
 __global__ void token_scatter_kernel(const int32_t* __restrict__ pairs, int n, int32_t* __restrict__ arena) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    arena[pairs[2 * i]] = pairs[2 * i + 1];
+    if (pairs[2 * i] >= 0) arena[pairs[2 * i]] = pairs[2 * i + 1];
 }
 
 void launch_token_pairs(const int32_t* arena, const int32_t* outpos, int n, int32_t* pairs, cudaStream_t st) {

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TDPIPE_LIB", os.path.join(_HERE, "libtdpipe.so"))
 
 TD_OK, TD_EINVAL, TD_ENOMEM, TD_ECUDA, TD_ENCCL, TD_ERANGE, TD_ESTATE = 0, -1, -2, -3, -4, -5, -6
-TD_POLICY_TDPIPE, TD_POLICY_PPSB_PRIO, TD_POLICY_PPSB_ALT = 0, 1, 2
+TD_POLICY_TDPIPE, TD_POLICY_PPSB_PRIO, TD_POLICY_PPSB_ALT, TD_POLICY_PPHB = 0, 1, 2, 3
 TD_EXEC_CUDA, TD_EXEC_NULL = 0, 1
 TD_BATCH_PREFILL, TD_BATCH_DECODE = 0, 1
 
@@ -36,7 +36,7 @@ class td_options(C.Structure):
                 ("eq2_bubble_scale", C.c_int32), ("weight_seed", C.c_uint64),
                 ("profile_csv", C.c_char_p), ("log_decisions", C.c_int32), ("record_logits", C.c_int32),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_ids", C.c_void_p),
-                ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32)]
+                ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32), ("hb_tokens", C.c_int32)]
 
 
 class td_run_stats(C.Structure):

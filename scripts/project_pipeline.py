@@ -17,7 +17,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2506_10470_b200 import (TD_EXEC_NULL, TD_POLICY_PPSB_ALT, TD_POLICY_PPSB_PRIO,  # noqa: E402
+from paper_2506_10470_b200 import (TD_EXEC_NULL, TD_POLICY_PPSB_ALT, TD_POLICY_PPHB, TD_POLICY_PPSB_PRIO,  # noqa: E402
                                    TD_POLICY_TDPIPE, TDPipe)
 from workload import SHAPES, config_workload  # noqa: E402
 
@@ -55,7 +55,8 @@ def run(cfg_name, model, S, kv_cap=None, out=None):
     C = kv_cap or stage_kv_blocks(shape, S)
     big = dataclasses.replace(shape, max_seq_len=8192)
     for name, pol, sigma in [("tdpipe", TD_POLICY_TDPIPE, 1), ("tdpipe_sigma", TD_POLICY_TDPIPE, max(1, S - 1)),
-                             ("ppsb_alt", TD_POLICY_PPSB_ALT, 1), ("ppsb_prio", TD_POLICY_PPSB_PRIO, 1)]:
+                             ("ppsb_alt", TD_POLICY_PPSB_ALT, 1), ("ppsb_prio", TD_POLICY_PPSB_PRIO, 1),
+                             ("pphb", TD_POLICY_PPHB, 1)]:
         if name == "tdpipe_sigma" and S <= 2:
             continue
         t = TDPipe(big, S, executor=TD_EXEC_NULL, kv_blocks=C, profile_csv=prof, policy=pol, eq2_bubble_scale=sigma,

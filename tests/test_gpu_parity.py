@@ -178,6 +178,38 @@ def test_td_run_evictions_teacher_forced(tmp_path):
     assert "E" in kinds
 
 
+def test_td_run_pphb_chunked_prefill_teacher_forced(tmp_path):
+    """PP+HB baseline [R23] on the GPU: hybrid micro-batches mixing decode
+    tokens and prefill chunks that attend to their paged prefix (small
+    hb_tokens so prompts split over several micro-batches, tight KV so
+    recompute evictions happen).  Logits teacher-forced vs the oracle, decision
+    log bit-exact vs oracle/scheduler.py."""
+    from oracle.scheduler import PPHB
+    from paper_2506_10470_b200 import TD_POLICY_PPHB
+    csv = str(tmp_path / "p.csv")
+    tables = synthetic_profile(64, 2048, knee=8)
+    write_profile_csv(csv, *tables)
+    kinds, n_chunk = set(), 0
+    for shape, seed, W, hb in [(SHAPES["tiny_gqa"].with_layers(2), 4, 2, 16), (SHAPES["tiny"], 9, 1, 7),
+                               (ModelShape("hd64", 2, 256, 4, 2, 512, 512, max_seq_len=512), 12, 2, 24)]:
+        Wt = OracleWeights(shape)
+        wl = random_tiny_workload(seed, vocab=shape.vocab, n_max=10, len_max=60)
+        need = max((len(r.prompt) + r.max_new_tokens + 15) // 16 for r in wl.requests)
+        C = need * W + 2
+        st, toks, logits, log = _tiny_run(shape, wl, W, csv, kv_blocks=C, policy=TD_POLICY_PPHB, hb_tokens=hb)
+        reqs = [(len(r.prompt), r.predicted_len, r.max_new_tokens) for r in wl.requests]
+        ref = schedule(reqs, SchedOptions(n_stages=W, block_size=16, kv_blocks=C, policy=PPHB, hb_tokens=hb), *tables)
+        assert log == "".join(l + "\n" for l in ref.log)
+        kinds |= {l.split()[0] for l in ref.log}
+        n_chunk += sum(1 for mb in ref.plan for q0, ql in zip(mb.q_start, mb.q_len) if ql > 1 and q0 > 0)
+        for r, tk, lg in zip(wl.requests, toks, logits):
+            assert len(tk) == r.max_new_tokens and lg.shape == (r.max_new_tokens, shape.vocab)
+            ref_l = F.teacher_forced_logits(Wt, r.prompt, tk)
+            _rows_ok(lg, ref_l)
+            _argmax_ok(lg, ref_l)
+    assert n_chunk > 0 and "H" in kinds
+
+
 @pytest.mark.slow
 def test_llama7b_shaped_bench_launch_config():
     """Full-size Llama-2-7B layers (d 4096, F 11008, V 32000) at the bench's

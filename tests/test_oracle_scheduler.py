@@ -279,3 +279,56 @@ def test_single_stage_equals_pipeline_outputs():
                                             prefill_token_budget=64, fp_stride=4), tdec, tpre)
             outs.append([r.n_out for r in s.reqs])
     assert all(o == outs[0] for o in outs)
+
+
+def test_pphb_invariants():
+    """PP+HB [R23]: every prompt is prefilled by contiguous chunks 0..L, each
+    micro-batch holds <= hb_tokens tokens (decode tokens count one each), each
+    engine stays inside its KV quota, and every request emits exactly its N
+    tokens (recompute included)."""
+    from oracle.scheduler import PPHB
+    for seed in range(60):
+        rng = np.random.default_rng(seed)
+        n, W, hb = int(rng.integers(1, 14)), int(rng.integers(1, 4)), int(rng.choice([8, 32, 64]))
+        reqs = [(int(rng.integers(1, 90)), int(rng.integers(1, 20)), int(rng.integers(1, 25))) for _ in range(n)]
+        need = max(ceil_div(L + N, 16) for L, _, N in reqs)
+        C = need * W + int(rng.integers(0, need + 1))
+        s = schedule(reqs, SchedOptions(n_stages=W, kv_blocks=C, policy=PPHB, hb_tokens=hb))
+        assert [r.n_out for r in s.reqs] == [N for _, _, N in reqs]
+        quota = [C // W + (1 if e < C % W else 0) for e in range(W)]
+        held = {}
+        for mb in s.plan:
+            assert mb.kind == "H" and sum(mb.q_len) <= hb
+            assert all(m % W == mb.slot for m in mb.members)
+        for line in s.log:
+            f = line.split()
+            if f[0] in ("A",):
+                held.setdefault(int(f[1]), 0)
+                held[int(f[1])] += len(f) - 2
+            elif f[0] in ("F", "E"):
+                held[int(f[1])] = 0
+            per = [0] * W
+            for rid, b in held.items():
+                per[rid % W] += b
+            assert all(per[e] <= quota[e] for e in range(W)), (seed, line)
+        # chunks of one admission are contiguous: q_start = previous end
+        nxt = {}
+        for line in s.log:
+            f = line.split()
+            if f[0] == "E":
+                nxt.pop(int(f[1]), None)
+            if f[0] == "H":
+                for c in f[5 + int(f[3]):]:
+                    rid, q0, ql = map(int, c.split(":"))
+                    assert q0 == nxt.get(rid, 0), (seed, line)
+                    nxt[rid] = q0 + ql
+
+
+def test_pphb_tiny_example():
+    """Hand-checked: one engine, hb = 8, prompts 10 and 3, outputs 2 and 1.
+    mb0 = chunk 0:0:8; mb1 = chunk 0:8:2 (prompt 0 done -> first token) +
+    1:0:3 (done, first token = its only token); mb2 = decode of request 0."""
+    from oracle.scheduler import PPHB
+    s = schedule([(10, 2, 2), (3, 1, 1)], SchedOptions(n_stages=1, kv_blocks=100, policy=PPHB, hb_tokens=8))
+    H = [l for l in s.log if l.startswith("H")]
+    assert H == ["H 0 0 0 1 0:0:8", "H 1 0 0 2 0:8:2 1:0:3", "H 2 0 1 0 0"], H

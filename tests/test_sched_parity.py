@@ -25,14 +25,14 @@ def _run_both(wl, tmp_path, tag, **o):
                       max_batch_seqs=o["max_seqs"], fp_stride=o["stride"], fp_horizon=o["horizon"],
                       policy=o["policy"], steal=o["steal"], alg1_check_before_launch=o["cbl"],
                       eq2_bubble_scale=o["sigma"], p2d_kv_permille=o.get("kvp", 0),
-                      d2p_finish_permille=o.get("finp", 0))
+                      d2p_finish_permille=o.get("finp", 0), hb_tokens=o.get("hb", 512))
     ref = schedule(reqs, so, tdec, tpre)
     shape = dataclasses.replace(SHAPES["tiny"].with_layers(max(2, o["W"])), max_seq_len=4096)
     t = TDPipe(shape, o["W"], executor=TD_EXEC_NULL, block_size=o["B"], kv_blocks=o["C"],
                prefill_token_budget=o["budget"], max_batch_seqs=o["max_seqs"], fp_stride=o["stride"],
                fp_horizon=o["horizon"], policy=o["policy"], steal=o["steal"], alg1_check_before_launch=o["cbl"],
                eq2_bubble_scale=o["sigma"], profile_csv=csv, p2d_kv_permille=o.get("kvp", 0),
-               d2p_finish_permille=o.get("finp", 0))
+               d2p_finish_permille=o.get("finp", 0), hb_tokens=o.get("hb", 512))
     t.submit_workload(wl)
     st = t.td_run()
     got = t.td_get_log()
@@ -67,6 +67,33 @@ def test_parity_random_tiny_workloads(tmp_path):
             kinds.add(line.split()[0] + (line.split()[1] if line.startswith("S") else ""))
     for k in ["P", "G", "A", "F", "D", "R", "SP2D", "SD2P", "E", "W", "U", "X"]:
         assert k in kinds, (k, kinds)
+
+
+def test_parity_pphb_random(tmp_path):
+    """PP+HB baseline [R23]: 400 random tiny runs, C++ controller log == oracle
+    log byte for byte (chunk splits, admissions, evictions, finishes)."""
+    rng = np.random.default_rng(77)
+    kinds = set()
+    n_chunked = 0
+    for seed in range(2001, 2401):
+        wl = random_tiny_workload(seed, n_max=14, len_max=40)
+        W = int(rng.integers(1, 6))
+        B = int(rng.choice([1, 4, 16]))
+        need = max((len(r.prompt) + r.max_new_tokens + B - 1) // B for r in wl.requests)
+        C = int(need * W + rng.integers(0, 3 * need + 1))
+        o = dict(W=W, B=B, C=C, budget=2048, max_seqs=64, stride=32, horizon=64, policy=3, steal=1, cbl=0, sigma=1,
+                 tables=synthetic_profile(8, 32, knee=4), hb=int(rng.choice([1, 7, 16, 32, 512])))
+        got, want, st, ref, n_out = _run_both(wl, tmp_path, seed % 7, **o)
+        assert got == want, f"seed {seed} opts {o}\n--- first diff at line " + str(
+            next((i for i, (a, b) in enumerate(zip(got.splitlines(), want.splitlines())) if a != b), None))
+        assert n_out == [r.max_new_tokens for r in wl.requests]
+        for line in ref.log:
+            kinds.add(line.split()[0])
+            if line.startswith("H"):
+                n_chunked += sum(1 for x in line.split()[5:] if ":" in x and not x.split(":")[1] == "0")
+    for k in ["H", "A", "F", "R", "E"]:
+        assert k in kinds, (k, kinds)
+    assert n_chunked > 100   # prompts really are split over several micro-batches
 
 
 def test_parity_sharegpt_shaped(tmp_path):
