@@ -187,7 +187,7 @@ def run_ours(args):
     wl = config_workload(args.config)
     n_req = len(wl.requests)
     policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
-              "ppsb_alt": tp.TD_POLICY_PPSB_ALT}[args.policy]
+              "ppsb_alt": tp.TD_POLICY_PPSB_ALT, "pphb": tp.TD_POLICY_PPHB}[args.policy]
     t = TDPipe(shape, args.stages, device=0, policy=policy, eq2_bubble_scale=args.sigma)
     info = t.td_info()
     # frozen profile table for Eq.1/Eq.2, measured once, untimed
@@ -332,7 +332,7 @@ def run_ours_multiprocess(args, world, rank):
     wl = config_workload(args.config)
     n_req = len(wl.requests)
     policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
-              "ppsb_alt": tp.TD_POLICY_PPSB_ALT}[args.policy]
+              "ppsb_alt": tp.TD_POLICY_PPSB_ALT, "pphb": tp.TD_POLICY_PPHB}[args.policy]
     import ctypes
     idbuf = ctypes.create_string_buffer(ids[0], 256)
     t = TDPipe(shape, world, device=local, policy=policy, eq2_bubble_scale=args.sigma, world_size=world, rank=rank,
@@ -391,7 +391,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--model", default="llama2_7b")
     ap.add_argument("--stages", type=int, default=1)
-    ap.add_argument("--policy", default="tdpipe", choices=["tdpipe", "ppsb_prio", "ppsb_alt"])
+    ap.add_argument("--policy", default="tdpipe", choices=["tdpipe", "ppsb_prio", "ppsb_alt", "pphb"])
     ap.add_argument("--sigma", type=int, default=1)
     ap.add_argument("--no-timing", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

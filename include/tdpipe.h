@@ -125,7 +125,8 @@ typedef struct td_batch {
   int32_t n_seqs;
   const int32_t* seq_slot;      /* [n] request slot (0 .. max_requests-1), KV owner    */
   const int32_t* q_start;       /* [n] absolute position of the first new token        */
-  const int32_t* q_len;         /* [n] new tokens (prefill: L; decode: 1)              */
+  const int32_t* q_len;         /* [n] new tokens (prefill: L, or a chunk continuing at
+                                   q_start > 0 over the paged prefix; decode: 1)        */
   const int32_t* block_table;   /* [n * max_blocks] physical KV block ids              */
   int32_t max_blocks;
 } td_batch;

@@ -649,8 +649,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
         launches_++;
       }
     } else if (M.prefill) {
+      // (q_start > 0: chunked prefill over the paged prefix, td_stage_forward)
       PrefillAttnParams pp{q_, kvl, dm + M.o_seq, dm + M.o_pos, dm + M.o_bt, M.maxblk, ob_, T, H_, Hkv_, hd_,
-                           dm + M.o_ctx, dm + M.o_last, n, M.max_ctx, nullptr};
+                           dm + M.o_ctx, dm + M.o_last, n, M.max_ctx, dm + M.o_qs};
       const int ip = tbegin(cPreAttn);
       launch_prefill_attn(pp, st_);
       tend(ip, 0, 0);
@@ -991,7 +992,7 @@ td_status CudaEngine::stage_forward(int stage, const td_batch& b, const void* in
   for (int i = 0; i < n; ++i) {
     if (b.q_len[i] < 1 || b.q_start[i] < 0) { error = "bad q_len/q_start"; return TD_EINVAL; }
     if (b.kind == TD_BATCH_DECODE && b.q_len[i] != 1) { error = "decode q_len must be 1"; return TD_EINVAL; }
-    if (b.kind == TD_BATCH_PREFILL && b.q_start[i] != 0) { error = "prefill starts at 0"; return TD_EINVAL; }
+    if (b.kind == TD_BATCH_PREFILL && b.q_start[i] < 0) { error = "q_start < 0"; return TD_EINVAL; }
     T += b.q_len[i];
     maxctx = std::max(maxctx, b.q_start[i] + b.q_len[i]);
     if (maxctx > s_.max_seq_len) { error = "context > max_seq_len"; return TD_ERANGE; }

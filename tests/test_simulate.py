@@ -13,7 +13,7 @@ def test_simulate_matches_run_and_bounds(tmp_path):
     wl = generate_workload(200, 256, 7, in_max=500, out_max=400)
     shape = dataclasses.replace(SHAPES["tiny"].with_layers(8), max_seq_len=4096)
     for S in (1, 2, 4):
-        for pol in (0, 1, 2):
+        for pol in (0, 1, 2, 3):
             kw = dict(executor=TD_EXEC_NULL, kv_blocks=900 * S, profile_csv=csv, policy=pol)
             a = TDPipe(shape, S, **kw)
             a.submit_workload(wl)
@@ -55,3 +55,36 @@ def test_trace_export(tmp_path):
     bubble = 1 - busy / (4 * st["makespan_ns"] / 1e3)
     assert abs(bubble - st["bubble_frac"]) < 1e-3
     assert max(e["args"]["blocks"] for e in kv) <= 1200
+
+
+def test_simulate_pphb_cost_model(tmp_path):
+    """PP+HB micro-batches in the timed replay [R23]: every H micro-batch costs
+    max(P(T), D(1)) + D(n_dec) - D(1) on every stage (read back from the trace),
+    so with one stage and no host gap the makespan is the sum of those costs."""
+    import json
+    from oracle.scheduler import PPHB, SchedOptions, schedule
+    csv = str(tmp_path / "p.csv")
+    tdec, tpre = synthetic_profile(512, 2048, dec_base_ns=3_000_000, dec_per_req_ns=4_000, knee=96)
+    write_profile_csv(csv, tdec, tpre)
+    wl = generate_workload(60, 256, 11, in_max=300, out_max=200)
+    shape = dataclasses.replace(SHAPES["tiny"].with_layers(4), max_seq_len=4096)
+    t = TDPipe(shape, 1, executor=TD_EXEC_NULL, kv_blocks=2000, profile_csv=csv, policy=3, hb_tokens=256)
+    t.submit_workload(wl)
+    st = t.td_simulate(0)
+    path = str(tmp_path / "trace.json")
+    t.td_write_trace(path)
+    spans = [e for e in json.load(open(path))["traceEvents"] if e["ph"] == "X"]
+    ref = schedule([(len(r.prompt), r.predicted_len, r.max_new_tokens) for r in wl.requests],
+                   SchedOptions(n_stages=1, kv_blocks=2000, policy=PPHB, hb_tokens=256))
+    L = {}
+    want = []
+    for mb in ref.plan:
+        # decode members lead: q_start >= current prompt length (no evictions here)
+        nd = sum(1 for rid, q0 in zip(mb.members, mb.q_start) if q0 >= len(wl.requests[rid].prompt))
+        T = sum(mb.q_len)
+        cost = max(tpre[min(T, 2048)], tdec[1]) + (tdec[nd] - tdec[1] if nd else 0)
+        want.append(cost)
+    assert ref.stats["evicted"] == 0
+    got = [round(e["dur"] * 1e3) for e in sorted(spans, key=lambda e: e["ts"])]
+    assert got == want
+    assert st["makespan_ns"] == sum(want)
