@@ -490,7 +490,8 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
   if (decode) {
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, 288 / ctas));
+    static const int64_t target = getenv("TDPIPE_SPLIT_TARGET") ? atoi(getenv("TDPIPE_SPLIT_TARGET")) : 288;
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, target / ctas));
     while (splits > 1 && (K / 64) / splits < 4) --splits;
     while (splits > 1 && (int64_t)splits * T * ((N + 127) / 128 * 128) > ws_cap_) --splits;
   }

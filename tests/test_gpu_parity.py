@@ -276,6 +276,35 @@ def test_llama7b_shaped_bench_launch_config():
         _rows_ok(out2[i], ref[-1])
 
 
+@pytest.mark.slow
+def test_llama70b_shaped_layer_gqa8():
+    """C5 shape (Llama-2-70B: d 8192, H 64 / Hkv 8, F 28672, V 32000), one of
+    its 80 layers: a <= 2048-token ShareGPT-mix prefill micro-batch and a decode
+    step of all its sequences, i.e. the GQA-8 decode-attention kernel and the
+    wide decode / prefill GEMMs at full width; the shortest sequence is checked
+    against the fp64 oracle (generating this layer's weights in fp64 takes the
+    oracle ~1 min)."""
+    shape = SHAPES["llama2_70b"].with_layers(1)
+    wl = generate_workload(64, shape.vocab, 5)
+    lengths, prompts = [], []
+    for r in wl.requests:
+        if sum(lengths) + len(r.prompt) > 2048:
+            break
+        lengths.append(len(r.prompt))
+        prompts.append(r.prompt)
+    t = TDPipe(shape, 1, kv_blocks=2048)
+    bt = _paged([L + 2 for L in lengths])
+    out = t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * len(lengths), lengths, bt, np.concatenate(prompts))
+    nxt = np.argmax(out, -1).astype(np.int32)
+    out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * len(lengths), bt, nxt)
+    t.close()
+    W = OracleWeights(shape)
+    for i in sorted(range(len(lengths)), key=lambda i: lengths[i])[:1]:
+        ref = F.sequence_logits(W, np.concatenate([prompts[i], [nxt[i]]]))
+        _rows_ok(out[i], ref[-2])
+        _rows_ok(out2[i], ref[-1])
+
+
 def test_decode_attention_long_context_many_pages():
     """Long contexts (many KV pages per split, every ring slot reused several
     times) for MHA hd=128 and GQA: decode logits vs the oracle."""
