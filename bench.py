@@ -93,7 +93,7 @@ class ClockSampler:
 _ORACLE_W = {}
 
 
-def oracle_sample(shape_name="llama2_7b", layers=2, n_tokens=6):
+def oracle_sample(shape_name="llama2_7b", layers=2, n_tokens=48):
     """The oracle as it stands, on a bounded sample of the C2 workload: greedy
     decode of `n_tokens` tokens of request 0 through `layers` of the 32 layers,
     scaled to the full depth.  Weight generation is setup (cached, untimed).

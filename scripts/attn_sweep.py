@@ -12,11 +12,12 @@ import numpy as np
 sys.path.insert(0, ".")
 from paper_2506_10470_b200.tdpipe import td_bench_attn  # noqa: E402
 
-H, HKV, HD = 32, 32, 128
 PEAK = 6535.7
 tag = sys.argv[1] if len(sys.argv) > 1 else "v1"
+# Llama-2-7B heads (MHA) by default; "gqa8" = Llama-2-70B heads (H 64 / Hkv 8)
+H, HKV, HD = (64, 8, 128) if "gqa8" in tag else (32, 32, 128)
 rng = np.random.default_rng(0)
-for n in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+for n in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512):
     for dist in ("256", "1024", "3072", "mix"):
         if dist == "mix":
             ctx = np.clip(rng.lognormal(6.3, 0.8, n), 32, 4000).astype(np.int32)

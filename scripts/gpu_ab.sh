@@ -10,3 +10,4 @@ run t148 TDPIPE_SPLIT_TARGET=148
 run t444 TDPIPE_SPLIT_TARGET=444
 run t592 TDPIPE_SPLIT_TARGET=592
 timeout 600 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --policy pphb > gpurun_out/ab_bench_pphb.log 2>&1
+timeout 300 python scripts/attn_sweep.py gqa8 > gpurun_out/attn_sweep_gqa8.txt 2>&1
