@@ -313,34 +313,63 @@ def run_ours(args):
 def run_ours_multiprocess(args, world, rank):
     """N > 1: one process per GPU = one pipeline stage (torchrun).  The
     controller is replicated on every rank (decisions depend only on logical
-    events), the fp32 residual moves stage -> stage and the sampled tokens
-    last -> stage 0 over the library's own NCCL communicators.  torch.distributed
-    only distributes the NCCL ids and takes the max of the per-rank times."""
+    events); the fp32 residual moves stage -> stage and the sampled tokens
+    last -> stage 0 through the library's peer-store hand-off (CUDA-IPC
+    mailboxes over NVLink, stream-ordered flags; `--handoff nccl` = the NCCL
+    send/recv baseline).  torch.distributed (gloo, host only) carries the
+    library's allgather callback (IPC handles, KV-capacity min, profile max),
+    the barriers and the max over ranks of the per-rank device times.
+    TDPIPE_SAME_DEVICE=1 puts every rank on cuda:0 (single-GPU check of the
+    multi-process path; the KV pool is then capped by --kv-blocks)."""
     import torch
     import torch.distributed as dist
 
     import paper_2506_10470_b200 as tp
     from paper_2506_10470_b200 import TDPipe, td_nccl_ids
 
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    same = os.environ.get("TDPIPE_SAME_DEVICE") == "1"
+    local = 0 if same else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ids = [td_nccl_ids() if rank == 0 else None]
-    dist.broadcast_object_list(ids, src=0)
+    dist.init_process_group("gloo")
+
+    def gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    def max_over_ranks(v):
+        x = torch.tensor([float(v)], dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        return float(x.item())
+
+    def sum_over_ranks(v):
+        x = torch.tensor([float(v)], dtype=torch.float64)
+        dist.all_reduce(x)
+        return float(x.item())
+
+    extra = {}
+    if args.handoff == "nccl":
+        ids = [td_nccl_ids() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        import ctypes
+        idbuf = ctypes.create_string_buffer(ids[0], 256)
+        extra = dict(handoff=tp.TD_HANDOFF_NCCL, nccl_ids=ctypes.cast(idbuf, ctypes.c_void_p))
+    kvb = args.kv_blocks or (2048 if same else 0)
     peaks = load_peaks()
     shape = SHAPES[args.model]
     wl = config_workload(args.config)
     n_req = len(wl.requests)
     policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
               "ppsb_alt": tp.TD_POLICY_PPSB_ALT, "pphb": tp.TD_POLICY_PPHB}[args.policy]
-    import ctypes
-    idbuf = ctypes.create_string_buffer(ids[0], 256)
     t = TDPipe(shape, world, device=local, policy=policy, eq2_bubble_scale=args.sigma, world_size=world, rank=rank,
-               nccl_ids=ctypes.cast(idbuf, ctypes.c_void_p))
+               allgather=gather, kv_blocks=kvb, **extra)
+    info = t.td_info()
     L = np.array([len(r.prompt) for r in wl.requests])
     P = np.array([r.predicted_len for r in wl.requests])
     ctx_rep = int(L.sum() // n_req + (P.sum() // n_req) // 2)
+    t0 = time.perf_counter()
     t.td_profile(None, min(1024, max(n_req, 1)), 2048, ctx_rep)
+    prof_s = time.perf_counter() - t0
 
     def one_step():
         t.td_reset()
@@ -352,6 +381,7 @@ def run_ours_multiprocess(args, world, rank):
         torch.cuda.synchronize()
         return st
 
+    t.td_set_timing(False)
     for _ in range(args.warmup):
         one_step()
     sampler = ClockSampler(local) if rank == 0 else None
@@ -359,24 +389,64 @@ def run_ours_multiprocess(args, world, rank):
         sampler.start()
     stats = [one_step() for _ in range(args.steps)]
     clocks = sampler.stop() if sampler else None
-    dev = torch.tensor([sum(s["makespan_ns"] for s in stats) / 1e9], dtype=torch.float64, device="cuda")
-    dist.all_reduce(dev, op=dist.ReduceOp.MAX)
-    dev_s = float(dev.item())
+    dev_s = max_over_ranks(sum(s["makespan_ns"] for s in stats) / 1e9)
     gen = sum(s["generated_tokens"] for s in stats)
-    launches = torch.tensor([sum(s["gpu_launches"] for s in stats)], dtype=torch.int64, device="cuda")
-    dist.all_reduce(launches)
+    launches = int(sum_over_ranks(sum(s["gpu_launches"] for s in stats)))
+    # instrumented pass: per-kernel CUDA events on every rank; bubble from the
+    # per-rank stage busy time (PAPER.md:454 reading R19)
+    kern, bubble = {}, None
+    if not args.no_timing:
+        t.td_set_timing(True)
+        kst = [one_step() for _ in range(args.steps)]
+        t.td_set_timing(False)
+        span = max_over_ranks(sum(s["makespan_ns"] for s in kst) / 1e6)
+        busy = sum_over_ranks(t.td_get_timing("stage")["ms"])
+        bubble = 100.0 * (1.0 - busy / (world * span)) if span > 0 else None
+        for name in ["decode_attn", "prefill_attn", "gemm_qkv_dec", "gemm_o_dec", "gemm_gu_dec", "gemm_down_dec",
+                     "lm_head_dec", "gemm_qkv_pre", "gemm_o_pre", "gemm_gu_pre", "gemm_down_pre", "lm_head_pre"]:
+            kern[name] = t.td_get_timing(name)   # this rank's stage
+    # e2e through the public API: prompts H2D, run, outputs D2H (stage 0)
+    e2e = []
+    for _ in range(max(1, min(args.steps, 2))):
+        t.td_reset()
+        dist.barrier()
+        torch.cuda.synchronize()
+        s0 = time.perf_counter()
+        t.submit_workload(wl)
+        t.td_upload()
+        st = t.td_run()
+        if rank == 0:
+            t.td_get_outputs(n_req, int(max(r.max_new_tokens for r in wl.requests)))
+        e2e.append(st["generated_tokens"] / max_over_ranks(time.perf_counter() - s0))
     if rank == 0:
+        arena = int(sum(len(r.prompt) + r.max_new_tokens + 1 for r in wl.requests) * 4)
         line = {"metric": METRIC, "value": gen / dev_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": f"{args.config}: {shape.name} random-init, {n_req} ShareGPT-length requests, "
-                                       f"{world}-stage TD-Pipe ({args.policy}), one process per GPU",
-                           "model": shape.name, "n_requests": n_req, "parallelism": f"pp{world}",
-                           "l2": "inputs larger than L2"},
-                "gpu_launches": int(launches.item()), "clocks": clocks,
-                "sched": {k: stats[-1][k] for k in ["n_microbatches", "n_p2d", "n_d2p", "n_stolen", "n_evicted"]},
-                "e2e": None, "roofline": None}
+                "config": dict(workload_config(args, world), kv_blocks=info["kv_blocks"], handoff=args.handoff,
+                               same_device=same, profile_s=round(prof_s, 2)),
+                "bubble_pct": bubble, "gpu_launches": launches, "clocks": clocks,
+                "sched": {k: stats[-1][k] for k in ["n_microbatches", "n_prefill_mb", "n_decode_mb", "n_p2d",
+                                                    "n_d2p", "n_stolen", "n_evicted", "prompt_tokens",
+                                                    "generated_tokens"]},
+                "e2e": {"value": statistics.mean(e2e), "unit": UNIT, "h2d_bytes_per_step": arena,
+                        "d2h_bytes_per_step": arena}}
+        main = {k: v for k, v in kern.items() if v["ms"] > 0}
+        if main:
+            dom = max(main, key=lambda k: main[k]["ms"])
+            d = main[dom]
+            if dom.endswith("_pre") or dom == "prefill_attn":
+                ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
+                line["roofline"] = {"kernel": dom + " (stage 0)", "bound": "tensor", "achieved": round(ach, 1),
+                                    "peak": peaks["tc_sus"], "unit": "TFLOP/s", "frac": round(ach / peaks["tc_sus"], 4),
+                                    "traffic": None, "peak_src": peaks["src"] + " (bf16 sustained)"}
+            else:
+                ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+                line["roofline"] = {"kernel": dom + " (stage 0)", "bound": "hbm", "achieved": round(ach, 1),
+                                    "peak": peaks["hbm"], "unit": "GB/s", "frac": round(ach / peaks["hbm"], 4),
+                                    "traffic": None, "peak_src": peaks["src"]}
         print(json.dumps(line), flush=True)
+    dist.barrier()
     t.close()
     dist.destroy_process_group()
     return 0
@@ -395,6 +465,8 @@ def main():
     ap.add_argument("--sigma", type=int, default=1)
     ap.add_argument("--no-timing", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--handoff", default="peer", choices=["peer", "nccl"])
+    ap.add_argument("--kv-blocks", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

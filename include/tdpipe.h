@@ -54,6 +54,27 @@ typedef int32_t td_status;
 #define TD_EXEC_CUDA 0
 #define TD_EXEC_NULL 1
 
+/* Stage hand-off in the multi-process pipeline (one process per GPU).
+ * PEER = the library's own peer-store path ("a single
+ * point-to-point communication"): every rank exports one device "mailbox"
+ * allocation through CUDA IPC; stage s stores its fp32 residual [T, d] straight
+ * into stage s+1's receive ring over NVLink, the last stage stores (arena
+ * position, token) pairs into stage 0's token ring, and readiness / slot reuse
+ * is signalled with 32-bit sequence flags written and waited on by the GPU
+ * streams themselves (stream memory operations; no host round trip, no SM
+ * spinning).  Needs `allgather` (host all-gather used for the IPC handles, the
+ * KV-capacity min and the profile-table max).  NCCL = ncclSend/ncclRecv on two
+ * library-owned communicators (needs nccl_ids); kept as the baseline. */
+#define TD_HANDOFF_PEER 0
+#define TD_HANDOFF_NCCL 1
+
+/* Host all-gather across the ranks of a multi-process pipeline: every rank
+ * passes `bytes` bytes in `send`; on return `recv` holds world_size * bytes,
+ * rank r's contribution at offset r * bytes.  Returns 0 on success.  Provided
+ * by the caller (e.g. torch.distributed over gloo); called only from td_create
+ * and td_profile, on the calling thread, in the same order on every rank. */
+typedef int32_t (*td_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+
 /* Model shape (Llama-style pre-norm decoder; Table 2). */
 typedef struct td_model_shape {
   int32_t n_layers;
@@ -94,6 +115,10 @@ typedef struct td_options {
   int32_t p2d_kv_permille;      /* P->D once allocated KV >= x/1000 of C */
   int32_t d2p_finish_permille;  /* D->P once x/1000 of the decode cohort finished */
   int32_t hb_tokens;            /* PPHB: tokens per hybrid micro-batch (default 512)   */
+  /* multi-process stage hand-off */
+  int32_t handoff;              /* TD_HANDOFF_PEER (default) | TD_HANDOFF_NCCL          */
+  td_allgather_fn allgather;    /* PEER: host all-gather (see td_allgather_fn)          */
+  void* allgather_user;         /* opaque first argument of allgather                  */
 } td_options;
 
 typedef struct td_run_stats {

@@ -71,6 +71,9 @@ extern "C" void td_default_options(td_options* o) {
   o->p2d_kv_permille = 0;
   o->d2p_finish_permille = 0;
   o->hb_tokens = 512;
+  o->handoff = TD_HANDOFF_PEER;
+  o->allgather = nullptr;
+  o->allgather_user = nullptr;
 }
 
 static bool read_profile(const std::string& path, std::vector<int64_t>* tdec, std::vector<int64_t>* tpre,
@@ -118,6 +121,10 @@ extern "C" td_status td_create(const td_model_shape* s, int32_t n_stages, const 
   if (c->opt.prefill_token_budget < 1 || c->opt.max_batch_seqs < 1 || c->opt.fp_stride < 1) return TD_EINVAL;
   if (c->opt.world_size < 1 || c->opt.rank < 0 || c->opt.rank >= c->opt.world_size) return TD_EINVAL;
   if (c->opt.world_size > 1 && c->opt.world_size != n_stages) return TD_EINVAL;
+  if (c->opt.handoff != TD_HANDOFF_PEER && c->opt.handoff != TD_HANDOFF_NCCL) return TD_EINVAL;
+  if (c->opt.executor != TD_EXEC_NULL && c->opt.world_size > 1 && c->opt.handoff == TD_HANDOFF_PEER &&
+      !c->opt.allgather)
+    return TD_EINVAL;
   if (!c->profile_path.empty()) {
     std::string e;
     if (!read_profile(c->profile_path, &c->tdec, &c->tpre, &e)) return TD_EINVAL;

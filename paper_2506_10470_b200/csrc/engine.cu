@@ -17,6 +17,7 @@
 //   arena    int32 tokens, request r at offset off[r]: prompt ++ generated
 //   work     x fp32 [T, d]; a bf16 [T, d]; q, o bf16 [T, H hd]; h bf16 [T, F];
 //            logits fp32 [n, V]; split-KV partials
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,6 +47,36 @@ namespace tdp {
   } while (0)
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Stream memory operations (driver API, resolved through the runtime so the
+// library does not link libcuda): a stream waits until a 32-bit flag reaches a
+// sequence number / writes one after all prior work (with a system-wide fence).
+typedef CUresult (*PfnStreamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PfnStreamValue32 g_wait32 = nullptr, g_write32 = nullptr;
+static bool load_stream_memops(std::string* err) {
+  if (g_wait32 && g_write32) return true;
+  void* a = nullptr;
+  void* b = nullptr;
+  cudaDriverEntryPointQueryResult qa, qb;
+  if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &a, 12000, cudaEnableDefault, &qa) != cudaSuccess ||
+      qa != cudaDriverEntryPointSuccess || !a ||
+      cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &b, 12000, cudaEnableDefault, &qb) != cudaSuccess ||
+      qb != cudaDriverEntryPointSuccess || !b) {
+    *err = "cuStreamWaitValue32/cuStreamWriteValue32 not available";
+    return false;
+  }
+  g_wait32 = reinterpret_cast<PfnStreamValue32>(a);
+  g_write32 = reinterpret_cast<PfnStreamValue32>(b);
+  return true;
+}
+
+// Peer-store mailbox layout (identical on every rank; include/tdpipe.h
+// TD_HANDOFF_PEER): [flags, 4 KB][token ring][residual receive ring].  Flags
+// are monotone 32-bit sequence numbers, one per 64-byte line.
+constexpr int kFlagRx = 0;       // residual slot seq filled by stage s-1  (written by s-1)
+constexpr int kFlagTxAck = 64;   // residual slot seq consumed by stage s+1 (written by s+1)
+constexpr int kFlagTok = 128;    // stage 0: token slot seq filled by the last stage
+constexpr int kFlagTokAck = 192; // last stage: token slot seq consumed by stage 0
 
 struct LayerW {
   bf16 *wqkv, *wo, *wgu, *wd, *g1, *g2;
@@ -108,7 +139,8 @@ class CudaEngine : public Engine {
   Meta build_meta(int r, bool prefill, int n, const int* q_start, const int* q_len, const int32_t* arena_off,
                   const char* emit,
                   const std::vector<const std::vector<int32_t>*>& blocks, const int32_t* bt_flat, int bt_stride);
-  td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena);
+  td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena, float* xpeer = nullptr,
+                      bool* sent = nullptr);
   td_status run_microbatch(const Meta& M, const int32_t* dmeta, int32_t* arena);
   td_status make_x_ops();
   int gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
@@ -138,6 +170,20 @@ class CudaEngine : public Engine {
   int32_t* pairs_ = nullptr;                 // last stage: [2 * capN]
   td_status nccl_check(int r, const char* what);
   td_status mp_send_recv_x(bool send, int peer, int T);
+  // peer-store hand-off (TD_HANDOFF_PEER)
+  bool peer_ = false;
+  char* mbox_ = nullptr;                 // own mailbox (exported through CUDA IPC)
+  std::map<int, char*> peer_mbox_;       // neighbours' mailboxes, opened here
+  static constexpr int kRx = 3;          // residual receive slots per boundary
+  int64_t rx_T_ = 0, tok_n_ = 0;         // rows per residual slot, pairs per token slot
+  int64_t tok_off_ = 0, rx_off_ = 0;
+  uint32_t fwd_out_ = 0, fwd_in_ = 0, tok_out_ = 0, tok_in_ = 0;   // monotone over the ctx lifetime
+  td_status peer_init();
+  td_status allgather(const void* send, void* recv, size_t bytes);
+  td_status flag_wait(cudaStream_t s, const char* base, int off, uint32_t v);
+  td_status flag_write(cudaStream_t s, char* base, int off, uint32_t v);
+  char* rx_slot(char* base, uint32_t seq) const { return base + rx_off_ + (int64_t)(seq % kRx) * rx_T_ * d_ * 4; }
+  char* tok_slot(char* base, uint32_t seq) const { return base + tok_off_ + (int64_t)(seq % kTokRing) * 2 * tok_n_ * 4; }
  public:
   int returned(const MicroBatch& mb) override;
  private:
@@ -240,7 +286,13 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   own_l0_ = stage_l0_[own_s0_];
   own_l1_ = stage_l1_[own_s1_ - 1];
   const bool has_embed = own_s0_ == 0, has_head = own_s1_ == S_;
-  if (world_ > 1) {
+  peer_ = world_ > 1 && o.handoff == TD_HANDOFF_PEER;
+  if (peer_) {
+    if (!o.allgather) { error = "TD_HANDOFF_PEER needs allgather"; return TD_EINVAL; }
+    if (!load_stream_memops(&error)) return TD_ECUDA;
+    CK(cudaStreamCreateWithFlags(&tst_, cudaStreamNonBlocking));
+    for (int i = 0; i < kTokRing; ++i) CK(cudaEventCreateWithFlags(&tok_ev_[i], cudaEventDisableTiming));
+  } else if (world_ > 1) {
 #ifdef TDP_NO_NCCL
     error = "built without nccl.h";
     return TD_ENCCL;
@@ -347,8 +399,13 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
     const double avail = (double)fr - o.hbm_reserve_frac * (double)tot - 512.0 * (1 << 20);
     C_ = (int64_t)(avail / (double)per_block);
   }
+  if (peer_) {   // one logical block table for all stages: C = min over ranks
+    std::vector<int64_t> all(world_);
+    if (td_status r3 = allgather(&C_, all.data(), sizeof(int64_t))) return r3;
+    C_ = *std::min_element(all.begin(), all.end());
+  }
 #ifndef TDP_NO_NCCL
-  if (world_ > 1) {   // one logical block table for all stages: C = min over ranks
+  if (world_ > 1 && !peer_) {   // one logical block table for all stages: C = min over ranks
     int64_t* dC = nullptr;
     CK(cudaMalloc(&dC, sizeof(int64_t)));
     CK(cudaMemcpyAsync(dC, &C_, sizeof(int64_t), cudaMemcpyHostToDevice, st_));
@@ -361,6 +418,8 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   if (C_ < 1) { error = "no room for the KV pool"; return TD_ENOMEM; }
   if (cudaMalloc(&kv_, C_ * per_block) != cudaSuccess) { error = "KV pool allocation failed"; return TD_ENOMEM; }
   CK(cudaMemsetAsync(kv_, 0, C_ * per_block, st_));
+  if (peer_)
+    if (td_status e3 = peer_init()) return e3;
   CK(cudaEventCreate(&ev_start_));
   CK(cudaEventCreate(&ev_end_));
   for (int i = 0; i < kRing; ++i) CK(cudaEventCreateWithFlags(&ring_ev_[i], cudaEventDisableTiming));
@@ -370,6 +429,17 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
 
 void CudaEngine::release() {
   if (st_) cudaStreamSynchronize(st_);
+  if (tst_) cudaStreamSynchronize(tst_);
+  if (peer_ && mbox_) {
+    // every rank is done storing into its neighbours' mailboxes before any is freed
+    int one = 1;
+    std::vector<int> all(world_);
+    allgather(&one, all.data(), sizeof one);
+    for (auto& kv : peer_mbox_) cudaIpcCloseMemHandle(kv.second);
+    peer_mbox_.clear();
+    cudaFree(mbox_);
+    mbox_ = nullptr;
+  }
   cudaFree(wbuf_);
   cudaFree(kv_);
   cudaFree(rope_);
@@ -597,7 +667,9 @@ bool CudaEngine::get_timing(const std::string& name, KernelTiming* t) {
 }
 
 // ------------------------------------------------------------------ forward
-td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int32_t* arena) {
+td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int32_t* arena, float* xpeer,
+                                bool* sent) {
+  if (sent) *sent = false;
   const int T = M.T, n = M.n;
   const int nqkv = (H_ + 2 * Hkv_) * hd_;
   const float eps = s_.rms_eps;
@@ -694,10 +766,15 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
-      const bf16* gnext = l + 1 < stage_l1_[stage] ? L_[l + 1].g1 : nullptr;
-      launch_resid_norm(ws_, sd, x_, gnext, a_, T, d_, eps, st_);
+      const bool last_layer = l + 1 == stage_l1_[stage];
+      const bf16* gnext = !last_layer ? L_[l + 1].g1 : nullptr;
+      // the stage's final residual rows are also stored straight into the
+      // next stage's receive slot (peer store over NVLink; no separate send)
+      float* xp = last_layer ? xpeer : nullptr;
+      launch_resid_norm(ws_, sd, x_, gnext, a_, T, d_, eps, st_, xp);
       launches_++;
       normed = gnext != nullptr;
+      if (xp && sent) *sent = true;
     }
   }
   if (stage == S_ - 1) {
@@ -719,16 +796,50 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
 }
 
 td_status CudaEngine::run_microbatch(const Meta& M, const int32_t* dm, int32_t* arena) {
+  const int64_t nx = (int64_t)M.T * d_;
+  if (peer_ && (M.T > rx_T_ || M.n > tok_n_)) { error = "micro-batch exceeds the hand-off slots"; return TD_ERANGE; }
   for (int s = own_s0_; s < own_s1_; ++s) {
-    if (world_ > 1 && s > 0)   // receive the fp32 residual hand-off from stage s-1
+    if (peer_ && s > 0) {
+      // residual hand-off from stage s-1: wait for slot `seq`, take it, free it
+      const uint32_t seq = ++fwd_in_;
+      if (td_status e = flag_wait(st_, mbox_, kFlagRx, seq)) return e;
+      launch_copy_f32(x_, reinterpret_cast<const float*>(rx_slot(mbox_, seq)), nx, st_);
+      launches_++;
+      if (td_status e = flag_write(st_, peer_mbox_.at(rank_ - 1), kFlagTxAck, seq)) return e;
+    } else if (world_ > 1 && s > 0) {   // receive the fp32 residual hand-off from stage s-1
       if (td_status e = mp_send_recv_x(false, s - 1, M.T)) return e;
+    }
+    float* xpeer = nullptr;
+    if (peer_ && s < S_ - 1) {   // reserve slot `seq` of stage s+1 (free once it consumed seq - kRx)
+      const uint32_t seq = ++fwd_out_;
+      if (seq > (uint32_t)kRx)
+        if (td_status e = flag_wait(st_, mbox_, kFlagTxAck, seq - kRx)) return e;
+      xpeer = reinterpret_cast<float*>(rx_slot(peer_mbox_.at(rank_ + 1), seq));
+    }
     const int is = tbegin(cStage);
-    if (td_status e = run_stage(s, M, dm, arena)) return e;
+    bool sent = false;
+    if (td_status e = run_stage(s, M, dm, arena, xpeer, &sent)) return e;
     tend(is, 0, 0);
-    if (world_ > 1 && s < S_ - 1)
+    if (peer_ && s < S_ - 1) {
+      if (!sent) {   // the stage did not end in a split-K reduce: store the rows now
+        launch_copy_f32(xpeer, x_, nx, st_);
+        launches_++;
+      }
+      if (td_status e = flag_write(st_, peer_mbox_.at(rank_ + 1), kFlagRx, fwd_out_)) return e;
+    } else if (world_ > 1 && s < S_ - 1) {
       if (td_status e = mp_send_recv_x(true, s + 1, M.T)) return e;
+    }
+    if (peer_ && s == S_ - 1) {   // sampled tokens -> stage 0's token ring (peer stores)
+      const uint32_t k = ++tok_out_;
+      if (k > (uint32_t)kTokRing)
+        if (td_status e = flag_wait(st_, mbox_, kFlagTokAck, k - kTokRing)) return e;
+      launch_token_pairs(arena, dm + M.o_outpos, M.n, reinterpret_cast<int32_t*>(tok_slot(peer_mbox_.at(0), k)),
+                         st_);
+      launches_++;
+      if (td_status e = flag_write(st_, peer_mbox_.at(0), kFlagTok, k)) return e;
+    }
 #ifndef TDP_NO_NCCL
-    if (world_ > 1 && s == S_ - 1) {   // sampled tokens -> stage 0 (token-return comm)
+    if (world_ > 1 && !peer_ && s == S_ - 1) {   // sampled tokens -> stage 0 (token-return comm)
       launch_token_pairs(arena, dm + M.o_outpos, M.n, pairs_, st_);
       if (td_status e = nccl_check(nc_->send(pairs_, (size_t)2 * M.n, ncclInt32, 0, cb_, st_), "ncclSend(tokens)"))
         return e;
@@ -769,6 +880,18 @@ td_status CudaEngine::mp_send_recv_x(bool send, int peer, int T) {
 // every rank): receive (position, token) pairs on the token stream, scatter
 // into the arena, and let the compute stream wait on it before its next launch.
 int CudaEngine::returned(const MicroBatch& mb) {
+  if (peer_ && own_s0_ == 0) {
+    const int n = (int)mb.members.size();
+    const uint32_t k = ++tok_in_;
+    const int slot = (int)(tok_k_ % kTokRing);
+    if (flag_wait(tst_, mbox_, kFlagTok, k)) return TD_ECUDA;
+    launch_token_scatter(reinterpret_cast<const int32_t*>(tok_slot(mbox_, k)), n, arena_, tst_);
+    if (flag_write(tst_, peer_mbox_.at(S_ - 1), kFlagTokAck, k)) return TD_ECUDA;
+    cudaEventRecord(tok_ev_[slot], tst_);
+    tok_have_ = true;
+    ++tok_k_;
+    return 0;
+  }
 #ifndef TDP_NO_NCCL
   if (world_ > 1 && own_s0_ == 0) {
     const int n = (int)mb.members.size();
@@ -1094,8 +1217,18 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
     kval.push_back(ns);
   }
   timing_ = saved;
+  if (peer_) {   // every rank must hold the same frozen table: per-stage max over ranks
+    std::vector<int64_t> mine(bval);
+    mine.insert(mine.end(), kval.begin(), kval.end());
+    std::vector<int64_t> all(mine.size() * world_);
+    if (td_status r = allgather(mine.data(), all.data(), mine.size() * sizeof(int64_t))) return r;
+    for (int rr = 0; rr < world_; ++rr)
+      for (size_t i = 0; i < mine.size(); ++i) mine[i] = std::max(mine[i], all[rr * mine.size() + i]);
+    std::copy(mine.begin(), mine.begin() + bval.size(), bval.begin());
+    std::copy(mine.begin() + bval.size(), mine.end(), kval.begin());
+  }
 #ifndef TDP_NO_NCCL
-  if (world_ > 1) {   // every rank must hold the same frozen table: per-stage max over ranks
+  if (world_ > 1 && !peer_) {   // every rank must hold the same frozen table: per-stage max over ranks
     std::vector<int64_t> all(bval);
     all.insert(all.end(), kval.begin(), kval.end());
     int64_t* dv = nullptr;
@@ -1129,6 +1262,66 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
   CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * (own_l1_ - own_l0_), st_));
   CK(cudaStreamSynchronize(st_));
   return TD_OK;
+}
+
+// ------------------------------------------------------ peer-store hand-off
+td_status CudaEngine::allgather(const void* send, void* recv, size_t bytes) {
+  if (!o_.allgather || o_.allgather(o_.allgather_user, send, recv, bytes) != 0) {
+    error = "allgather callback failed";
+    return TD_EINVAL;
+  }
+  return TD_OK;
+}
+
+td_status CudaEngine::flag_wait(cudaStream_t s, const char* base, int off, uint32_t v) {
+  const CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(base + off), v,
+                              CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) { error = "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")"; return TD_ECUDA; }
+  return TD_OK;
+}
+
+td_status CudaEngine::flag_write(cudaStream_t s, char* base, int off, uint32_t v) {
+  // default flags: the value becomes visible only after every prior store of
+  // the stream (including peer stores over NVLink) -- a release
+  const CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(base + off), v,
+                               CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) { error = "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")"; return TD_ECUDA; }
+  return TD_OK;
+}
+
+// Every rank allocates one mailbox with the same layout, exports it through
+// CUDA IPC, and opens the mailboxes of the ranks it stores into: s+1 (residual
+// + its flag), s-1 (slot-free acks), and for stages 0 / S-1 each other (token
+// ring, token acks).  Slot capacities are fixed here from the options, so no
+// mailbox is ever reallocated (a micro-batch over them fails with TD_ERANGE).
+td_status CudaEngine::peer_init() {
+  rx_T_ = std::max<int64_t>({(int64_t)o_.prefill_token_budget, (int64_t)s_.max_seq_len,
+                             (int64_t)o_.max_batch_seqs + std::max(o_.hb_tokens, 0)});
+  tok_n_ = (int64_t)o_.max_batch_seqs + std::max(o_.hb_tokens, 0);
+  tok_off_ = 4096;
+  rx_off_ = tok_off_ + cdiv((int64_t)kTokRing * 2 * tok_n_ * 4, 4096) * 4096;
+  const int64_t bytes = rank_ == 0 ? rx_off_ : rx_off_ + (int64_t)kRx * rx_T_ * d_ * 4;
+  CK(cudaMalloc(&mbox_, bytes));
+  CK(cudaMemset(mbox_, 0, 4096));
+  CK(cudaDeviceSynchronize());
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, mbox_));
+  std::vector<cudaIpcMemHandle_t> all(world_);
+  if (td_status e = allgather(&h, all.data(), sizeof h)) return e;
+  std::vector<int> need;
+  if (rank_ > 0) need.push_back(rank_ - 1);
+  if (rank_ < S_ - 1) need.push_back(rank_ + 1);
+  if (rank_ == 0) need.push_back(S_ - 1);
+  if (rank_ == S_ - 1) need.push_back(0);
+  for (int r : need) {
+    if (r == rank_ || peer_mbox_.count(r)) continue;
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+    peer_mbox_[r] = static_cast<char*>(p);
+  }
+  int one = 1;   // every mailbox is open (and its flags zeroed) before anyone stores into it
+  std::vector<int> ok(world_);
+  return allgather(&one, ok.data(), sizeof one);
 }
 
 // ------------------------------------------------------------------ factory

@@ -41,8 +41,12 @@ void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* row
 // Fused split-K reduction + residual add + next RMSNorm (decode GEMMs whose
 // epilogue is a residual add):  x[t] += sum_s ws[s][t] (split order), then, if
 // g != nullptr, out[t] = bf16(RMSNorm(x[t]) * g).
+// xpeer (nullable): also store the updated residual rows there (stage hand-off
+// into the next stage's receive slot, a CUDA-IPC peer pointer)
 void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
-                       cudaStream_t st);
+                       cudaStream_t st, float* xpeer = nullptr);
+// dst[0, n) = src[0, n) (fp32, n % 4 == 0); dst may be a peer (IPC) pointer
+void launch_copy_f32(float* dst, const float* src, int64_t n, cudaStream_t st);
 // tokens: arena[outpos[i]] = argmax_j logits[i][j] (lowest index on ties)
 void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int32_t* outpos, cudaStream_t st);
 // multi-process token return: pairs[2i] = outpos[i], pairs[2i+1] = arena[outpos[i]]; and its inverse

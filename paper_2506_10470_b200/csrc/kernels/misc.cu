@@ -6,6 +6,7 @@
 #include <float.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 
 #include <cooperative_groups.h>
@@ -155,11 +156,12 @@ void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* row
 template <int NT>
 __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict__ ws, int splits, float* __restrict__ x,
                                                         const bf16* __restrict__ g, bf16* __restrict__ out, int T,
-                                                        int d, float eps) {
+                                                        int d, float eps, float* __restrict__ xpeer) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x;
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)t * d);
+  float4* xp = xpeer ? reinterpret_cast<float4*>(xpeer + (int64_t)t * d) : nullptr;
   __shared__ float red[NT / 32];
   float ss = 0.f;
   for (int j = threadIdx.x; j < d / 4; j += NT) {
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict_
     v.z += acc.z;
     v.w += acc.w;
     xr[j] = v;
+    if (xp) xp[j] = v;   // stage hand-off: the same row stored into the next stage's receive slot
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   if (!g) return;
@@ -210,7 +213,8 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict_
 template <int RC>
 __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __restrict__ ws, int splits,
                                                                   float* __restrict__ x, const bf16* __restrict__ g,
-                                                                  bf16* __restrict__ out, int T, int d, float eps) {
+                                                                  bf16* __restrict__ out, int T, int d, float eps,
+                                                                  float* __restrict__ xpeer) {
   pdl_trigger();
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
@@ -219,6 +223,7 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
   const int per = d / RC;                      // elements of this CTA's slice
   const int j0 = rank * per / 4;               // float4 index
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)t * d);
+  float4* xp = xpeer ? reinterpret_cast<float4*>(xpeer + (int64_t)t * d) : nullptr;
   __shared__ float red[4];
   __shared__ float part_ss;
   float ss = 0.f;
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
     v.z += acc.z;
     v.w += acc.w;
     xr[j] = v;
+    if (xp) xp[j] = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   ss = warp_sum(ss);
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
 }
 
 void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
-                       cudaStream_t st) {
+                       cudaStream_t st, float* xpeer) {
   if (T <= 0) return;
   if (T <= 64 && d % (8 * 4) == 0) {
     cudaLaunchConfig_t cfg = {};
@@ -279,9 +285,9 @@ void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf1
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<8>, ws, splits, x, g, out, T, d, eps);
+    cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<8>, ws, splits, x, g, out, T, d, eps, xpeer);
   } else {
-    launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps);
+    launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps, xpeer);
   }
 }
 
@@ -378,6 +384,24 @@ void launch_token_pairs(const int32_t* arena, const int32_t* outpos, int n, int3
 void launch_token_scatter(const int32_t* pairs, int n, int32_t* arena, cudaStream_t st) {
   if (n <= 0) return;
   token_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(pairs, n, arena);
+}
+
+
+// ------------------------------------------------------- stage hand-off copy
+// fp32 row block copy, 16-byte vectors; with a peer (CUDA IPC) destination the
+// stores travel over NVLink straight into the next stage's receive slot.
+__global__ void copy_f32_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcg(src + i);
+}
+void launch_copy_f32(float* dst, const float* src, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t n4 = n / 4;   // n = T * d, d % 64 == 0
+  const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+  launch_k(copy_f32_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<float4*>(dst),
+           reinterpret_cast<const float4*>(src), n4);
 }
 
 }  // namespace tdp

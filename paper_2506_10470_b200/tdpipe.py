@@ -19,6 +19,10 @@ TD_OK, TD_EINVAL, TD_ENOMEM, TD_ECUDA, TD_ENCCL, TD_ERANGE, TD_ESTATE = 0, -1, -
 TD_POLICY_TDPIPE, TD_POLICY_PPSB_PRIO, TD_POLICY_PPSB_ALT, TD_POLICY_PPHB = 0, 1, 2, 3
 TD_EXEC_CUDA, TD_EXEC_NULL = 0, 1
 TD_BATCH_PREFILL, TD_BATCH_DECODE = 0, 1
+TD_HANDOFF_PEER, TD_HANDOFF_NCCL = 0, 1
+
+# int32 (*)(void* user, const void* send, void* recv, size_t bytes) -- include/tdpipe.h td_allgather_fn
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
 
 
 class td_model_shape(C.Structure):
@@ -36,7 +40,8 @@ class td_options(C.Structure):
                 ("eq2_bubble_scale", C.c_int32), ("weight_seed", C.c_uint64),
                 ("profile_csv", C.c_char_p), ("log_decisions", C.c_int32), ("record_logits", C.c_int32),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_ids", C.c_void_p),
-                ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32), ("hb_tokens", C.c_int32)]
+                ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32), ("hb_tokens", C.c_int32),
+                ("handoff", C.c_int32), ("allgather", ALLGATHER_FN), ("allgather_user", C.c_void_p)]
 
 
 class td_run_stats(C.Structure):
@@ -135,12 +140,31 @@ def make_shape(shape) -> td_model_shape:
                           shape.vocab, float(shape.rope_theta), float(shape.rms_eps), shape.max_seq_len)
 
 
+def make_allgather(gather):
+    """Wrap `gather(bytes) -> list[bytes]` (this rank's bytes in, every rank's
+    bytes out in rank order -- e.g. torch.distributed.all_gather_object) as the
+    td_allgather_fn callback of td_options.allgather."""
+    def cb(user, send, recv, nbytes):
+        try:
+            parts = gather(C.string_at(send, nbytes))
+            buf = b"".join(parts)
+            C.memmove(recv, buf, len(buf))
+            return 0
+        except Exception:   # no exception may cross the C ABI
+            import traceback
+            traceback.print_exc()
+            return -1
+    return ALLGATHER_FN(cb)
+
+
 def default_options(**kw) -> td_options:
     o = td_options()
     lib().td_default_options(C.byref(o))
     for k, v in kw.items():
         if k == "profile_csv" and isinstance(v, str):
             v = v.encode()
+        if k == "allgather" and not isinstance(v, ALLGATHER_FN):
+            v = make_allgather(v)
         setattr(o, k, v)
     return o
 
@@ -153,6 +177,7 @@ class TDPipe:
         self._keep = []
         o = default_options(**opts)
         self._keep.append(o.profile_csv)
+        self._keep.append(o)   # holds the allgather callback, which must outlive the ctx (td_destroy calls it)
         self.ctx = C.c_void_p()
         st = lib().td_create(C.byref(make_shape(shape)), int(n_stages), C.byref(o), C.byref(self.ctx))
         if st != TD_OK:
