@@ -564,6 +564,12 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
     splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, target / ctas));
     while (splits > 1 && (K / 64) / splits < 4) --splits;
     while (splits > 1 && (int64_t)splits * T * ((N + 127) / 128 * 128) > ws_cap_) --splits;
+    // A/B knobs: cap the split count of the QKV GEMM (its reduce is a separate
+    // RoPE / KV-scatter kernel) or of the residual GEMMs (reduced in resid_norm)
+    static const int cap_qkv = getenv("TDPIPE_SPLITS_QKV") ? atoi(getenv("TDPIPE_SPLITS_QKV")) : 8;
+    static const int cap_res = getenv("TDPIPE_SPLITS_RESID") ? atoi(getenv("TDPIPE_SPLITS_RESID")) : 8;
+    if (ep.mode == kEpiQKV) splits = std::max(1, std::min(splits, cap_qkv));
+    if (ep.mode == kEpiResid) splits = std::max(1, std::min(splits, cap_res));
   }
   const int used = launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, counters_, decode, st_, defer);
   launches_ += (used > 1 && !defer) ? 2 : 1;
@@ -670,6 +676,20 @@ bool CudaEngine::get_timing(const std::string& name, KernelTiming* t) {
 td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int32_t* arena, float* xpeer,
                                 bool* sent) {
   if (sent) *sent = false;
+  // A/B knobs (decode micro-batches of >= X tokens launch without PDL):
+  // whole micro-batch / attention + its successor / GEMMs
+  static const int nopdl_t = getenv("TDPIPE_NOPDL_T") ? atoi(getenv("TDPIPE_NOPDL_T")) : 1 << 30;
+  static const int nopdl_attn = getenv("TDPIPE_NOPDL_ATTN_T") ? atoi(getenv("TDPIPE_NOPDL_ATTN_T")) : 1;
+  static const int nopdl_gemm = getenv("TDPIPE_NOPDL_GEMM_T") ? atoi(getenv("TDPIPE_NOPDL_GEMM_T")) : 1 << 30;
+  const bool big = !M.prefill && M.T >= nopdl_t;
+  static const int nopdl_o = getenv("TDPIPE_NOPDL_O_T") ? atoi(getenv("TDPIPE_NOPDL_O_T")) : 1 << 30;
+  const bool big_attn = !M.prefill && M.T >= nopdl_attn;
+  const bool big_o = !M.prefill && M.T >= nopdl_o;
+  const bool big_gemm = !M.prefill && M.T >= nopdl_gemm;
+  pdl_suppress(big);
+  struct Restore {
+    ~Restore() { pdl_suppress(false); }
+  } restore_pdl;
   const int T = M.T, n = M.n;
   const int nqkv = (H_ + 2 * Hkv_) * hd_;
   const float eps = s_.rms_eps;
@@ -700,7 +720,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ep.hd = hd_;
     const int iq = tbegin(cQKV + (M.prefill ? 0 : kDecOff));
     if (iq >= 0 && !M.prefill) timed_[iq].sub = kGemmBucket + bucket_of(T);
+    if (big_gemm) pdl_suppress(true);
     gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec);
+    pdl_suppress(big);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.hybrid) {
       // PP+HB: decode members [0, nd) -- one token each, so token row = member
@@ -710,7 +732,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
         DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, M.nd, H_, Hkv_, hd_, 0,
                             attn_cnt_};
         plan_decode_attn(dp, mb_ctx_.data());
+        if (M.nd >= nopdl_attn) pdl_suppress(true);
         launch_decode_attn(dp, st_);
+        pdl_suppress(big);
         launches_++;
       }
       if (M.nd < n) {
@@ -735,7 +759,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       plan_decode_attn(dp, mb_ctx_.data());
       const int ida = tbegin(cDecAttn);
       if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
+      if (big_attn) pdl_suppress(true);
       launch_decode_attn(dp, st_);
+      pdl_suppress(big);
       tend(ida, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
       launches_++;
     }
@@ -745,7 +771,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eo.ldo = d_;
     const int io = tbegin(cO + (M.prefill ? 0 : kDecOff));
     if (io >= 0 && !M.prefill) timed_[io].sub = kGemmBucket + bucket_of(T);
+    if (big_o || big_gemm) pdl_suppress(true);
     const int so = gemm(xo_, w.to, T, d_, H_ * hd_, eo, dec, /*defer=*/true);
+    pdl_suppress(big);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
     if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
     else launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
@@ -755,7 +783,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eg.out_bf16 = h_;
     const int ig = tbegin(cGU + (M.prefill ? 0 : kDecOff));
     if (ig >= 0 && !M.prefill) timed_[ig].sub = kGemmBucket + bucket_of(T);
+    if (big_gemm) pdl_suppress(true);
     gemm(xa_, w.tgu, T, 2 * F_, d_, eg, dec);
+    pdl_suppress(big);
     tend(ig, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
     EpiParams ed{};
     ed.mode = kEpiResid;
@@ -763,7 +793,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ed.ldo = d_;
     const int idn = tbegin(cDown + (M.prefill ? 0 : kDecOff));
     if (idn >= 0 && !M.prefill) timed_[idn].sub = kGemmBucket + bucket_of(T);
+    if (big_gemm) pdl_suppress(true);
     const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
+    pdl_suppress(big);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
       const bool last_layer = l + 1 == stage_l1_[stage];

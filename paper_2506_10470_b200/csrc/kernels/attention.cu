@@ -241,7 +241,7 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
 template <int HD, int G>
 __global__ void __launch_bounds__(128)
 decode_attn_kernel(DecodeAttnParams p) {
-  pdl_trigger();
+  pdl_trigger_tail(G == 1 ? 4 : G <= 4 ? 3 : 2);   // resident CTAs per SM (registers)
   // ctx / block tables are host-uploaded metadata (complete before the
   // previous kernel ran): read before the PDL wait, which attend_range takes
   const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
   uint8_t* sQ = fsm;
   uint8_t* sK = fsm + TILE;          // 2 stages
   uint8_t* sV = fsm + 3 * TILE;      // 2 stages
-  pdl_trigger();
+  pdl_trigger_tail(2);
   pdl_wait();
   const int qt = blockIdx.x, seq = blockIdx.y, h = blockIdx.z;
   const int L = p.seq_ctx[seq];                  // keys: positions 0 .. L-1

@@ -151,8 +151,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* accf = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
 
-
-  pdl_trigger();
+  pdl_trigger_tail(BN <= 128 ? 2 : 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid: x = token tile (fastest, so CTAs sharing a weight tile run together
   // and the re-read hits L2), y = 128-row weight tile, z = K split
@@ -298,7 +297,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__
   uint64_t* accf = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
 
-  pdl_trigger();
+  pdl_trigger_tail(1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128;              // tokens
   const int n0 = blockIdx.y * BNF;              // features

@@ -6,6 +6,9 @@
 
 namespace tdp {
 
+// launches from this host thread go without the PDL attribute while on (misc.cu)
+void pdl_suppress(bool on);
+
 typedef __nv_bfloat16 bf16;
 
 // ---- weight init (F9 counter-based recipe), physical layouts -------------

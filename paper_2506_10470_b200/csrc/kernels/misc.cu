@@ -18,13 +18,16 @@ namespace cg = cooperative_groups;
 
 namespace tdp {
 
+static thread_local int g_pdl_suppress = 0;
+void pdl_suppress(bool on) { g_pdl_suppress = on ? 1 : 0; }
+
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = std::getenv("TDPIPE_PDL");
     on = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
   }
-  return on == 1;
+  return on == 1 && !g_pdl_suppress;
 }
 
 // splitmix64 finaliser (counter-based; both sides implement it independently)
@@ -84,7 +87,7 @@ void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st) {
 // ----------------------------------------------------------------- embedding
 __global__ void embed_kernel(const int32_t* __restrict__ arena, const int32_t* __restrict__ tok_idx,
                              const bf16* __restrict__ E, float* __restrict__ x, int d) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   const int t = blockIdx.x;
   const int tok = arena[tok_idx[t]];
@@ -109,7 +112,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
                                                      bf16* __restrict__ out, const int32_t* __restrict__ rows,
                                                      int d, float eps) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   const int i = blockIdx.x;
   const int r = rows ? rows[i] : i;
@@ -157,7 +160,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict__ ws, int splits, float* __restrict__ x,
                                                         const bf16* __restrict__ g, bf16* __restrict__ out, int T,
                                                         int d, float eps, float* __restrict__ xpeer) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   const int t = blockIdx.x;
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)t * d);
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
                                                                   float* __restrict__ x, const bf16* __restrict__ g,
                                                                   bf16* __restrict__ out, int T, int d, float eps,
                                                                   float* __restrict__ xpeer) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   const int t = blockIdx.y;
@@ -294,7 +297,7 @@ void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf1
 // -------------------------------------------------------------------- argmax
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ arena,
                               const int32_t* __restrict__ outpos) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   const int i = blockIdx.x;
   const float* l = logits + (int64_t)i * V;
@@ -363,7 +366,7 @@ void launch_argmax(const float* logits, int n, int V, int32_t* arena, const int3
 // last stage: (arena position, token) pairs of one micro-batch -> NCCL to stage 0
 __global__ void token_pairs_kernel(const int32_t* __restrict__ arena, const int32_t* __restrict__ outpos, int n,
                                    int32_t* __restrict__ pairs) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int p = outpos[i];
@@ -391,7 +394,7 @@ void launch_token_scatter(const int32_t* pairs, int n, int32_t* arena, cudaStrea
 // fp32 row block copy, 16-byte vectors; with a peer (CUDA IPC) destination the
 // stores travel over NVLink straight into the next stage's receive slot.
 __global__ void copy_f32_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4) {
-  pdl_trigger();
+  pdl_trigger_tail(8);
   pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = __ldcg(src + i);
