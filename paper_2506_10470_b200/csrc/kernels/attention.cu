@@ -111,14 +111,36 @@ __device__ __forceinline__ void attn_finish(const DecodeAttnParams& p, int seq, 
     const int g = e / HD, dim = e % HD;
     const int h = kh * G + g;
     const float* part = p.part + ((int64_t)seq * H + h) * p.max_splits * (HD + 2);
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < n_splits; ++s2) M = fmaxf(M, __ldcg(part + s2 * (HD + 2)));
-    float L = 0.f, A = 0.f;
-    for (int s2 = 0; s2 < n_splits; ++s2) {
-      const float* ps = part + s2 * (HD + 2);
-      const float c = exp2f(__ldcg(ps) - M);
-      L += __ldcg(ps + 1) * c;
-      A += __ldcg(ps + 2 + dim) * c;
+    // up to 8 splits' partials are loaded at once (one L2 round trip per 8
+    // splits instead of two dependent loads per split), then combined in
+    // split order; with <= 8 splits the arithmetic is the two-pass
+    // global-max form exactly
+    float M = -INFINITY, L = 0.f, A = 0.f;
+    for (int s0 = 0; s0 < n_splits; s0 += 8) {
+      float mv[8], lv[8], av[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool ok = s0 + j < n_splits;
+        const float* ps = part + (s0 + j) * (HD + 2);
+        mv[j] = ok ? __ldcg(ps) : -INFINITY;
+        lv[j] = ok ? __ldcg(ps + 1) : 0.f;
+        av[j] = ok ? __ldcg(ps + 2 + dim) : 0.f;
+      }
+      float mn = M;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mn = fmaxf(mn, mv[j]);
+      if (M != -INFINITY) {
+        const float c0 = exp2f(M - mn);
+        L *= c0;
+        A *= c0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float c = mv[j] == -INFINITY ? 0.f : exp2f(mv[j] - mn);
+        L += lv[j] * c;
+        A += av[j] * c;
+      }
+      M = mn;
     }
     p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
   }
