@@ -682,6 +682,8 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
   static const int nopdl_attn = getenv("TDPIPE_NOPDL_ATTN_T") ? atoi(getenv("TDPIPE_NOPDL_ATTN_T")) : 1;
   static const int nopdl_gemm = getenv("TDPIPE_NOPDL_GEMM_T") ? atoi(getenv("TDPIPE_NOPDL_GEMM_T")) : 1 << 30;
   const bool big = !M.prefill && M.T >= nopdl_t;
+  // timing-only experiment (wrong results): skip the split-K reduction kernels
+  static const bool skip_red = getenv("TDPIPE_SKIP_REDUCE") && atoi(getenv("TDPIPE_SKIP_REDUCE"));
   static const int nopdl_o = getenv("TDPIPE_NOPDL_O_T") ? atoi(getenv("TDPIPE_NOPDL_O_T")) : 1 << 30;
   const bool big_attn = !M.prefill && M.T >= nopdl_attn;
   const bool big_o = !M.prefill && M.T >= nopdl_o;
@@ -721,7 +723,11 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     const int iq = tbegin(cQKV + (M.prefill ? 0 : kDecOff));
     if (iq >= 0 && !M.prefill) timed_[iq].sub = kGemmBucket + bucket_of(T);
     if (big_gemm) pdl_suppress(true);
-    gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec);
+    // pure decode: the QKV split-K reduction (+ RoPE + K/V write) is left to
+    // the attention kernel (DecodeAttnParams::qkv_ws) -- one launch fewer
+    static const bool fuse_qkv = !getenv("TDPIPE_FUSE_QKV") || atoi(getenv("TDPIPE_FUSE_QKV"));
+    const bool defer_qkv = dec && !M.hybrid && (fuse_qkv || skip_red);
+    const int qsplits = gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec, /*defer=*/defer_qkv);
     pdl_suppress(big);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.hybrid) {
@@ -756,6 +762,12 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     } else {
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, n, H_, Hkv_, hd_, 0,
                           attn_cnt_};
+      if (defer_qkv && qsplits > 1) {
+        dp.qkv_ws = ws_;
+        dp.qkv_splits = qsplits;
+        dp.nqkv = nqkv;
+        dp.rope_cs = rope_;
+      }
       plan_decode_attn(dp, mb_ctx_.data());
       const int ida = tbegin(cDecAttn);
       if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
@@ -775,7 +787,8 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     const int so = gemm(xo_, w.to, T, d_, H_ * hd_, eo, dec, /*defer=*/true);
     pdl_suppress(big);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
-    if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
+    if (so > 1 && skip_red) {
+    } else if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
     else launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
     launches_++;
     EpiParams eg{};
@@ -797,7 +810,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
     pdl_suppress(big);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
-    if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
+    if (sd > 1 && skip_red) {
+      normed = l + 1 < stage_l1_[stage];
+    } else if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
       const bool last_layer = l + 1 == stage_l1_[stage];
       const bf16* gnext = !last_layer ? L_[l + 1].g1 : nullptr;
       // the stage's final residual rows are also stored straight into the

@@ -200,21 +200,74 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
   // tail of the QKV kernel.  After the wait, the thread holding the newest
   // token (written by that kernel) reloads it through L2 (ld.cg: the
   // pre-wait load may have left a stale line in L1), and q is read.
+  const bool fused = p.qkv_ws != nullptr;
+  // fused mode: the newest token's k / v do not exist yet (they are in the
+  // QKV partials); it is left out of the streamed range and added last
+  const bool has_new = fused && newest >= t_begin && newest < t_end;
+  if (has_new) t_end = newest;
   issue(t_begin, kr, vr, valid);
   pdl_wait();
+  __shared__ __align__(16) bf16 s_qkv[(G + 2) * HD];
+  if (fused) {
+    // the QKV split-K epilogue, done cooperatively (all loads in flight at
+    // once): q of the G heads of kv head kh, plus k / v of the newest token
+    // when this CTA holds it; sum in split order, RoPE at position ctx-1 on
+    // the interleaved (i, i+hd/2) pairs, bf16 -- as splitk_reduce_kernel
+    const int npairs = (G + (has_new ? 2 : 0)) * (HD / 2);
+    for (int pi = threadIdx.x; pi < npairs; pi += NW * 32) {
+      const int e = pi * 2;
+      int f;
+      bool rope = true;
+      if (e < G * HD) f = kh * G * HD + e;
+      else if (e < (G + 1) * HD) f = (H + kh) * HD + (e - G * HD);
+      else { f = (H + p.Hkv + kh) * HD + (e - (G + 1) * HD); rope = false; }
+      float2 pr[8];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int t = t_begin + (u * NW + warp) * TPW + tg;
-    if (t == newest) {
-      const int64_t kb = (((int64_t)bt[t >> 4] * 2) * p.Hkv + kh) * head_stride + (t & 15) * HD + sub * 8;
-      kr[u] = __ldcg(reinterpret_cast<const uint4*>(p.kv + kb));
-      vr[u] = __ldcg(reinterpret_cast<const uint4*>(p.kv + kb + (int64_t)p.Hkv * head_stride));
+      for (int s2 = 0; s2 < 8; ++s2)
+        if (s2 < p.qkv_splits)
+          pr[s2] = __ldcg(reinterpret_cast<const float2*>(p.qkv_ws + ((int64_t)s2 * p.n + seq) * p.nqkv + f));
+      const float2 cs = rope ? *reinterpret_cast<const float2*>(p.rope_cs + ((int64_t)newest * (HD >> 1) + ((f % HD) >> 1)) * 2)
+                             : make_float2(1.f, 0.f);
+      float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+        if (s2 < p.qkv_splits) { v0 += pr[s2].x; v1 += pr[s2].y; }
+      for (int s2 = 8; s2 < p.qkv_splits; ++s2) {
+        const float2 q2 = __ldcg(reinterpret_cast<const float2*>(p.qkv_ws + ((int64_t)s2 * p.n + seq) * p.nqkv + f));
+        v0 += q2.x;
+        v1 += q2.y;
+      }
+      float r0 = v0, r1 = v1;
+      if (rope) {
+        r0 = v0 * cs.x - v1 * cs.y;
+        r1 = v1 * cs.x + v0 * cs.y;
+      }
+      *reinterpret_cast<uint32_t*>(s_qkv + e) = pack_bf16x2(r0, r1);
+    }
+    __syncthreads();
+    if (has_new && warp == 0 && tg == 0) {   // the new token's K / V into the paged cache
+      const int64_t kb = (((int64_t)bt[newest >> 4] * 2) * p.Hkv + kh) * head_stride + (newest & 15) * HD + sub * 8;
+      bf16* kvw = const_cast<bf16*>(p.kv);
+      *reinterpret_cast<uint4*>(kvw + kb) = *reinterpret_cast<const uint4*>(s_qkv + G * HD + sub * 8);
+      *reinterpret_cast<uint4*>(kvw + kb + (int64_t)p.Hkv * head_stride) =
+          *reinterpret_cast<const uint4*>(s_qkv + (G + 1) * HD + sub * 8);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t_begin + (u * NW + warp) * TPW + tg;
+      if (t == newest) {
+        const int64_t kb = (((int64_t)bt[t >> 4] * 2) * p.Hkv + kh) * head_stride + (t & 15) * HD + sub * 8;
+        kr[u] = __ldcg(reinterpret_cast<const uint4*>(p.kv + kb));
+        vr[u] = __ldcg(reinterpret_cast<const uint4*>(p.kv + kb + (int64_t)p.Hkv * head_stride));
+      }
     }
   }
   float q[G][8];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p.q + ((int64_t)seq * H + kh * G + g) * HD + sub * 8);
+    const uint4 u = fused ? *reinterpret_cast<const uint4*>(s_qkv + g * HD + sub * 8)
+                          : *reinterpret_cast<const uint4*>(p.q + ((int64_t)seq * H + kh * G + g) * HD + sub * 8);
     bf16x8_to_f32(u, q[g]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) q[g][i] *= scale;
@@ -254,6 +307,28 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
         }
       } else {
         issue(base + STEP, kr, vr, valid);
+      }
+    }
+  }
+  if (has_new && warp == 0) {   // fused mode: the newest token, by thread group 0 of warp 0
+    float kf[8], vf[8];
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(s_qkv + G * HD + sub * 8), kf);
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(s_qkv + (G + 1) * HD + sub * 8), vf);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float sc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sc = fmaf(q[g][i], kf[i], sc);
+#pragma unroll
+      for (int o = LPT / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+      if (tg == 0) {
+        const float mn = fmaxf(m[g], sc);
+        const float corr = exp2f(m[g] - mn);
+        const float pr = exp2f(sc - mn);
+        l[g] = l[g] * corr + pr;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[g][i] = fmaf(pr, vf[i], acc[g][i] * corr);
+        m[g] = mn;
       }
     }
   }
@@ -517,7 +592,7 @@ static bool v2_enabled() {   // TDPIPE_ATTN_V2=1: smem page-ring kernel (measure
 template <int HD>
 static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
   const int G = p.H / p.Hkv;
-  if (v2_enabled()) {
+  if (v2_enabled() && !p.qkv_ws) {
     switch (G) {
       case 1: launch_v2<HD, 1>(p, st); return;
       case 2: launch_v2<HD, 2>(p, st); return;

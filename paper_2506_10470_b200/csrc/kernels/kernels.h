@@ -88,6 +88,14 @@ struct DecodeAttnParams {
   int n, H, Hkv, hd;
   int split_tokens;      // context tokens per split (multiple of 16)
   int* counters;         // [n * Hkv] zero-initialised split tickets (reset by the merging CTA)
+  // Fused QKV split-K reduction: when set, the QKV GEMM left its split partials
+  // unreduced in qkv_ws[s][seq][f] (f < nqkv); every CTA sums its q heads from
+  // them in split order and applies RoPE at position ctx-1, and the CTA holding
+  // the newest token does the same for its k / v and writes them to the paged
+  // cache -- the work of the separate split-K epilogue kernel, bit for bit
+  const float* qkv_ws = nullptr;
+  int qkv_splits = 0, nqkv = 0;
+  const float* rope_cs = nullptr;   // [max_pos][hd/2][2] (cos, sin)
 };
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 // Launch plan from the host copy of the context lengths: sets split_tokens
