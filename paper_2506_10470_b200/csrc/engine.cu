@@ -556,7 +556,8 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
   int splits = 1;
   // 129..256-token decode batches of the wide GEMMs (QKV, gate/up, LM head) are
   // closer to the tensor roof than to HBM: take the token-major kernel
-  if (decode && T > 128 && N >= 8192) decode = false;
+  static const bool dec_tn = !getenv("TDPIPE_DEC_TN") || atoi(getenv("TDPIPE_DEC_TN"));   // A/B knob
+  if (decode && T > 128 && N >= 8192 && dec_tn) decode = false;
   if (decode) {
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
