@@ -45,7 +45,10 @@ def load_peaks():
         d = json.load(open(p))
         return dict(hbm=d["hbm_gbs"], tc=d["bf16_tflops"], tc_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
                     src="measured (MEASURED_PEAKS.json)")
-    return dict(hbm=6650.0, tc=1590.0, tc_sus=1400.0, src="fallback (B200_PROFILING.md)")
+    # the driver writes MEASURED_PEAKS.json per pod; without it, the values it
+    # held on this pool in round 1 (recorded in profiles/README.md)
+    return dict(hbm=6535.7, tc=1673.3, tc_sus=1406.7,
+                src="MEASURED_PEAKS.json absent: this pool's round-1 measured peaks (profiles/README.md)")
 
 
 class ClockSampler:
