@@ -56,3 +56,26 @@ def test_submit_validation_and_null_run():
     assert st["generated_tokens"] == 8
     assert len(t.td_get_output(0)) == 5 and len(t.td_get_output(1)) == 3
     t.close()
+
+
+def test_options_layout_and_handoff_validation():
+    """td_options as seen through ctypes matches the C defaults (layout check of
+    the trailing multi-process fields) and the hand-off options are validated
+    before any device is touched."""
+    import ctypes as C
+    from paper_2506_10470_b200.tdpipe import TD_HANDOFF_NCCL, TD_HANDOFF_PEER, default_options, make_shape
+    o = default_options()
+    assert o.block_size == 16 and o.prefill_token_budget == 2048 and o.hb_tokens == 512
+    assert o.world_size == 1 and o.handoff == TD_HANDOFF_PEER and not o.allgather and not o.allgather_user
+    L = lib()
+    ctx = C.c_void_p()
+    s = make_shape(SHAPES["tiny"])
+    # CUDA executor, 2 ranks, peer hand-off without an allgather callback: TD_EINVAL
+    o2 = default_options(world_size=2, rank=0)
+    assert L.td_create(C.byref(s), 2, C.byref(o2), C.byref(ctx)) == -1
+    # unknown hand-off kind: TD_EINVAL
+    o3 = default_options(executor=TD_EXEC_NULL, handoff=7)
+    assert L.td_create(C.byref(s), 1, C.byref(o3), C.byref(ctx)) == -1
+    o4 = default_options(executor=TD_EXEC_NULL, handoff=TD_HANDOFF_NCCL)
+    assert L.td_create(C.byref(s), 1, C.byref(o4), C.byref(ctx)) == 0
+    L.td_destroy(ctx)

@@ -62,9 +62,24 @@ def _worker(rank, world, port, csv, seeds, q):
     import sys
     sys.path.insert(0, ROOT)
     from paper_2506_10470_b200 import TD_EXEC_NULL, TDPipe, td_nccl_ids
+    from paper_2506_10470_b200.tdpipe import make_allgather
     ids = [td_nccl_ids() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     out = {"ids": ids[0], "logs": []}
+    # (d) the td_allgather_fn callback the library calls in peer-store mode
+    # (IPC handles, KV-capacity min, profile max): rank order, exact bytes
+    import ctypes
+
+    def gather(b):
+        parts = [None] * world
+        dist.all_gather_object(parts, b)
+        return parts
+    cb = make_allgather(gather)
+    mine = bytes([rank + 1]) * 64 + rank.to_bytes(8, "little")
+    send = ctypes.create_string_buffer(mine, len(mine))
+    recv = ctypes.create_string_buffer(len(mine) * world)
+    out["allgather_rc"] = cb(None, ctypes.cast(send, ctypes.c_void_p), ctypes.cast(recv, ctypes.c_void_p), len(mine))
+    out["allgather"] = recv.raw
     for seed in seeds:
         wl = random_tiny_workload(seed, n_max=14, len_max=40)
         t = TDPipe(SHAPES["tiny"].with_layers(4), world, executor=TD_EXEC_NULL, kv_blocks=6, block_size=16,
@@ -98,6 +113,9 @@ def test_replicated_controllers_and_p2p_schedule(tmp_path, world):
         assert p.exitcode == 0
     # (c) ids intact on every rank
     assert all(g["ids"] == gathered[0]["ids"] and len(g["ids"]) == 256 for g in gathered)
+    # (d) allgather callback: every rank receives every rank's bytes in rank order
+    want = b"".join(bytes([r + 1]) * 64 + r.to_bytes(8, "little") for r in range(world))
+    assert all(g["allgather_rc"] == 0 and g["allgather"] == want for g in gathered)
     evictions = 0
     for i, seed in enumerate(seeds):
         logs = [g["logs"][i] for g in gathered]
