@@ -119,6 +119,9 @@ typedef struct td_options {
   int32_t handoff;              /* TD_HANDOFF_PEER (default) | TD_HANDOFF_NCCL          */
   td_allgather_fn allgather;    /* PEER: host all-gather (see td_allgather_fn)          */
   void* allgather_user;         /* opaque first argument of allgather                  */
+  /* roofline accounting (td_run_stats.ideal_ns): peaks of this device; 0 = off */
+  double hbm_peak_gbs;          /* HBM bandwidth, GB/s (measured copy bandwidth)        */
+  double tc_peak_tflops;        /* dense bf16 tensor-core TFLOP/s                       */
 } td_options;
 
 typedef struct td_run_stats {
@@ -140,6 +143,15 @@ typedef struct td_run_stats {
   int64_t h2d_bytes;
   int64_t d2h_bytes;
   int64_t busy_ns[8];           /* per-stage busy time (first 8 stages)                */
+  /* Speed-of-light accounting of this process's micro-batches:
+   * per micro-batch, algorithmic HBM bytes (every weight of its layers once,
+   * every context token's K and V per layer, the new K/V written) and FLOPs
+   * (2 x tokens x weights + causal attention); ideal_ns = sum over micro-batches
+   * of max(bytes / hbm_peak, flops / tc_peak) (0 if the peaks are not set).
+   * ideal_ns / makespan_ns is the whole job's roofline fraction. */
+  double ideal_ns;
+  double alg_bytes;
+  double alg_flops;
 } td_run_stats;
 
 /* A single micro-batch for td_stage_forward (testing entry point). */

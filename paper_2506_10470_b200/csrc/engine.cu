@@ -231,6 +231,7 @@ class CudaEngine : public Engine {
   float* hlogits_ = nullptr;
   int64_t hlogits_cap_ = 0;
   int64_t launches_ = 0, h2d_bytes_ = 0;
+  double ideal_ns_ = 0, alg_bytes_ = 0, alg_flops_ = 0;   // speed-of-light accounting of the run
   // timing
   bool timing_ = false;
   std::vector<TimedLaunch> timed_;
@@ -994,6 +995,7 @@ td_status CudaEngine::begin_run(const std::vector<HostReq>& reqs, bool record_lo
   record_ = record_logits;
   rec_.assign(record_logits ? reqs.size() : 0, {});
   launches_ = 0;
+  ideal_ns_ = alg_bytes_ = alg_flops_ = 0;
   timed_.clear();
   ev_used_ = 0;
   started_ = false;
@@ -1025,6 +1027,26 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
       if (ensure_work(T, n, mb_blk)) return TD_ECUDA;
       for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
     }
+  }
+  {   // algorithmic work of this micro-batch on this process's layers (td_run_stats.ideal_ns)
+    const int nl = own_l1_ - own_l0_;
+    const double nqkv = (double)(H_ + 2 * Hkv_) * hd_;
+    const double w_layer = 2.0 * (nqkv * d_ + (double)d_ * H_ * hd_ + 2.0 * F_ * d_ + (double)d_ * F_ + 2.0 * d_);
+    const bool head = own_s1_ == S_;
+    const double kv_tok = 2.0 * Hkv_ * hd_ * 2;   // K + V bytes per token per layer
+    double T = 0, ctx_sum = 0, att = 0;
+    for (int i = 0; i < n; ++i) {
+      const double qs = mb.q_start[i], ql = mb.q_len[i];
+      T += ql;
+      ctx_sum += qs + ql;
+      att += ql * (qs + (ql + 1) / 2);   // causal (query, key) pairs
+    }
+    const double bytes = nl * (w_layer + ctx_sum * kv_tok + T * kv_tok) + (head ? 2.0 * V_ * d_ + 2.0 * d_ : 0.0);
+    const double flops = nl * (T * w_layer + 4.0 * H_ * hd_ * att) + (head ? 2.0 * n * V_ * d_ : 0.0);
+    alg_bytes_ += bytes;
+    alg_flops_ += flops;
+    if (o_.hbm_peak_gbs > 0 && o_.tc_peak_tflops > 0)
+      ideal_ns_ += std::max(bytes / o_.hbm_peak_gbs, flops / (o_.tc_peak_tflops * 1e3));
   }
   const int r = ring_acquire();
   // PP+HB hybrid micro-batch: decode members (q_start >= L) lead, then chunks;
@@ -1123,6 +1145,9 @@ td_status CudaEngine::end_run(td_run_stats* st) {
   }
   st->gpu_launches = launches_;
   st->h2d_bytes = h2d_bytes_;
+  st->ideal_ns = ideal_ns_;
+  st->alg_bytes = alg_bytes_;
+  st->alg_flops = alg_flops_;
   return TD_OK;
 }
 

@@ -41,7 +41,8 @@ class td_options(C.Structure):
                 ("profile_csv", C.c_char_p), ("log_decisions", C.c_int32), ("record_logits", C.c_int32),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_ids", C.c_void_p),
                 ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32), ("hb_tokens", C.c_int32),
-                ("handoff", C.c_int32), ("allgather", ALLGATHER_FN), ("allgather_user", C.c_void_p)]
+                ("handoff", C.c_int32), ("allgather", ALLGATHER_FN), ("allgather_user", C.c_void_p),
+                ("hbm_peak_gbs", C.c_double), ("tc_peak_tflops", C.c_double)]
 
 
 class td_run_stats(C.Structure):
@@ -51,7 +52,8 @@ class td_run_stats(C.Structure):
                 ("n_microbatches", C.c_int64), ("n_prefill_mb", C.c_int64), ("n_decode_mb", C.c_int64),
                 ("n_p2d", C.c_int64), ("n_d2p", C.c_int64), ("n_stolen", C.c_int64),
                 ("n_evicted", C.c_int64), ("gpu_launches", C.c_int64), ("h2d_bytes", C.c_int64),
-                ("d2h_bytes", C.c_int64), ("busy_ns", C.c_int64 * 8)]
+                ("d2h_bytes", C.c_int64), ("busy_ns", C.c_int64 * 8), ("ideal_ns", C.c_double),
+                ("alg_bytes", C.c_double), ("alg_flops", C.c_double)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "busy_ns"}
