@@ -165,6 +165,21 @@ def workload_config(args, n_gpus=1):
             "l2": "inputs larger than L2 (weights + KV per step >> 126 MB)"}
 
 
+def job_roofline(stats, peaks):
+    """Whole-job speed of light: the engine's per-micro-batch
+    algorithmic bytes / FLOPs (td_run_stats), ideal = sum over micro-batches of
+    max(bytes / HBM peak, FLOPs / TC peak), divided by the measured makespan."""
+    ideal = sum(s["ideal_ns"] for s in stats)
+    span = sum(s["makespan_ns"] for s in stats)
+    n = max(len(stats), 1)
+    return {"frac": round(ideal / span, 4) if span else None, "ideal_ms_per_step": round(ideal / 1e6 / n, 2),
+            "ms_per_step": round(span / 1e6 / n, 2), "alg_bytes_per_step": sum(s["alg_bytes"] for s in stats) / n,
+            "alg_flops_per_step": sum(s["alg_flops"] for s in stats) / n, "peak_hbm_gbs": peaks["hbm"],
+            "peak_tc_tflops": peaks["tc_sus"],
+            "def": "sum_mb max(bytes/HBM, flops/TC) / makespan; bytes = weights once + K/V of every context "
+                   "token per layer + new K/V; flops = 2*tokens*weights + causal attention"}
+
+
 def _traffic_record(kernel):
     import glob
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*",
@@ -191,7 +206,8 @@ def run_ours(args):
     n_req = len(wl.requests)
     policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
               "ppsb_alt": tp.TD_POLICY_PPSB_ALT, "pphb": tp.TD_POLICY_PPHB}[args.policy]
-    t = TDPipe(shape, args.stages, device=0, policy=policy, eq2_bubble_scale=args.sigma)
+    t = TDPipe(shape, args.stages, device=0, policy=policy, eq2_bubble_scale=args.sigma,
+               hbm_peak_gbs=peaks["hbm"], tc_peak_tflops=peaks["tc_sus"])
     info = t.td_info()
     # frozen profile table for Eq.1/Eq.2, measured once, untimed
     L = np.array([len(r.prompt) for r in wl.requests])
@@ -268,6 +284,7 @@ def run_ours(args):
                                             "n_stolen", "n_evicted", "prompt_tokens", "generated_tokens"]},
         "clocks": clocks,
         "e2e": {"value": statistics.mean(e2e_vals), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "job_roofline": job_roofline(stats, peaks),
     }
     if kern:
         main = {k: v for k, v in kern.items() if "@" not in k}
@@ -365,7 +382,7 @@ def run_ours_multiprocess(args, world, rank):
     policy = {"tdpipe": tp.TD_POLICY_TDPIPE, "ppsb_prio": tp.TD_POLICY_PPSB_PRIO,
               "ppsb_alt": tp.TD_POLICY_PPSB_ALT, "pphb": tp.TD_POLICY_PPHB}[args.policy]
     t = TDPipe(shape, world, device=local, policy=policy, eq2_bubble_scale=args.sigma, world_size=world, rank=rank,
-               allgather=gather, kv_blocks=kvb, **extra)
+               allgather=gather, kv_blocks=kvb, hbm_peak_gbs=peaks["hbm"], tc_peak_tflops=peaks["tc_sus"], **extra)
     info = t.td_info()
     L = np.array([len(r.prompt) for r in wl.requests])
     P = np.array([r.predicted_len for r in wl.requests])
@@ -393,6 +410,8 @@ def run_ours_multiprocess(args, world, rank):
     stats = [one_step() for _ in range(args.steps)]
     clocks = sampler.stop() if sampler else None
     dev_s = max_over_ranks(sum(s["makespan_ns"] for s in stats) / 1e9)
+    # slowest stage's speed of light vs the pipeline makespan
+    ideal_s = max_over_ranks(sum(s["ideal_ns"] for s in stats) / 1e9)
     gen = sum(s["generated_tokens"] for s in stats)
     launches = int(sum_over_ranks(sum(s["gpu_launches"] for s in stats)))
     # instrumented pass: per-kernel CUDA events on every rank; bubble from the
@@ -433,7 +452,9 @@ def run_ours_multiprocess(args, world, rank):
                                                     "n_d2p", "n_stolen", "n_evicted", "prompt_tokens",
                                                     "generated_tokens"]},
                 "e2e": {"value": statistics.mean(e2e), "unit": UNIT, "h2d_bytes_per_step": arena,
-                        "d2h_bytes_per_step": arena}}
+                        "d2h_bytes_per_step": arena},
+                "job_roofline": {"frac": round(ideal_s / dev_s, 4) if dev_s else None,
+                                 "def": "max over stages of sum_mb max(bytes/HBM, flops/TC) / pipeline makespan"}}
         main = {k: v for k, v in kern.items() if v["ms"] > 0}
         if main:
             dom = max(main, key=lambda k: main[k]["ms"])

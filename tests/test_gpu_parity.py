@@ -324,3 +324,38 @@ def test_decode_attention_long_context_many_pages():
             ref = F.sequence_logits(W, np.concatenate([p, [nxt[i]]]))
             _rows_ok(out[i], ref[-2])
             _rows_ok(out2[i], ref[-1])
+
+
+def test_td_run_speed_of_light_accounting(tmp_path):
+    """td_run_stats.alg_bytes / alg_flops / ideal_ns (the whole-job roofline of
+    bench.py) equal the closed form for C1: every micro-batch streams all
+    weights once (+ the LM head), every context token's K/V per layer is read
+    and each new token's K/V written; FLOPs = 2 x tokens x weights + causal
+    attention + the LM head rows.  With oracle predictions and 64 blocks there
+    is no eviction, so the per-request contexts are 16 (prefill) and 17..31
+    (decode steps)."""
+    shape = SHAPES["tiny"]
+    wl = config_workload("C1")
+    csv = str(tmp_path / "p.csv")
+    write_profile_csv(csv, *synthetic_profile(64, 2048))
+    t = TDPipe(shape, 2, kv_blocks=64, profile_csv=csv, hbm_peak_gbs=6535.7, tc_peak_tflops=1406.7)
+    t.submit_workload(wl)
+    st = t.td_run()
+    t.close()
+    d, H, Hkv, F_, V, nl = shape.d_model, shape.n_heads, shape.n_kv_heads, shape.d_ffn, shape.vocab, shape.n_layers
+    hd = d // H
+    w_layer = 2.0 * ((H + 2 * Hkv) * hd * d + d * H * hd + 2 * F_ * d + d * F_ + 2 * d)
+    head = 2.0 * V * d + 2.0 * d
+    kv_tok = 2.0 * Hkv * hd * 2
+    n_req = len(wl.requests)
+    L, N = 16, 16
+    ctx_sum = n_req * (L + sum(L + k for k in range(1, N)))          # prefill ctx + decode contexts
+    new_tok = n_req * (L + N - 1)
+    att = n_req * (L * (L + 1) / 2 + sum(L + k for k in range(1, N)))
+    n_mb = st["n_microbatches"]
+    want_bytes = n_mb * (nl * w_layer + head) + nl * kv_tok * (ctx_sum + new_tok)
+    want_flops = nl * (new_tok * w_layer + 4.0 * H * hd * att) + 2.0 * n_req * N * V * d
+    assert st["n_evicted"] == 0
+    assert st["alg_bytes"] == pytest.approx(want_bytes, rel=1e-9)
+    assert st["alg_flops"] == pytest.approx(want_flops, rel=1e-9)
+    assert 0 < st["ideal_ns"] < st["makespan_ns"]
