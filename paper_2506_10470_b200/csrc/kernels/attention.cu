@@ -619,8 +619,11 @@ void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
   // page-ring kernel keeps 6 pages in flight per CTA, so it wants fewer,
   // longer CTAs: one resident wave of ~4 per SM
   const bool v2 = v2_enabled();
-  const int64_t target = (v2 ? 4 : 8) * 148;
-  int split = 512, max_ctx = 1;
+  // A/B knobs: CTA target per SM, largest split (tokens, power of two >= 128)
+  static const int tgt_env = std::getenv("TDPIPE_ATTN_TARGET") ? std::atoi(std::getenv("TDPIPE_ATTN_TARGET")) : 0;
+  static const int max_env = std::getenv("TDPIPE_ATTN_MAXSPLIT") ? std::atoi(std::getenv("TDPIPE_ATTN_MAXSPLIT")) : 0;
+  const int64_t target = (int64_t)(tgt_env > 0 ? tgt_env : (v2 ? 4 : 8)) * 148;
+  int split = max_env >= kAttnMinSplit ? max_env : 512, max_ctx = 1;
   for (int i = 0; i < p.n; ++i) max_ctx = std::max(max_ctx, ctx[i]);
   for (;;) {
     int64_t ctas = 0;
