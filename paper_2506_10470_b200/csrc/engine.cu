@@ -684,8 +684,6 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
   static const int nopdl_attn = getenv("TDPIPE_NOPDL_ATTN_T") ? atoi(getenv("TDPIPE_NOPDL_ATTN_T")) : 1;
   static const int nopdl_gemm = getenv("TDPIPE_NOPDL_GEMM_T") ? atoi(getenv("TDPIPE_NOPDL_GEMM_T")) : 1 << 30;
   const bool big = !M.prefill && M.T >= nopdl_t;
-  // timing-only experiment (wrong results): skip the split-K reduction kernels
-  static const bool skip_red = getenv("TDPIPE_SKIP_REDUCE") && atoi(getenv("TDPIPE_SKIP_REDUCE"));
   static const int nopdl_o = getenv("TDPIPE_NOPDL_O_T") ? atoi(getenv("TDPIPE_NOPDL_O_T")) : 1 << 30;
   const bool big_attn = !M.prefill && M.T >= nopdl_attn;
   const bool big_o = !M.prefill && M.T >= nopdl_o;
@@ -728,7 +726,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     // pure decode: the QKV split-K reduction (+ RoPE + K/V write) is left to
     // the attention kernel (DecodeAttnParams::qkv_ws) -- one launch fewer
     static const bool fuse_qkv = !getenv("TDPIPE_FUSE_QKV") || atoi(getenv("TDPIPE_FUSE_QKV"));
-    const bool defer_qkv = dec && !M.hybrid && (fuse_qkv || skip_red);
+    const bool defer_qkv = dec && !M.hybrid && fuse_qkv;
     const int qsplits = gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec, /*defer=*/defer_qkv);
     pdl_suppress(big);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
@@ -789,8 +787,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     const int so = gemm(xo_, w.to, T, d_, H_ * hd_, eo, dec, /*defer=*/true);
     pdl_suppress(big);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
-    if (so > 1 && skip_red) {
-    } else if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
+    if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
     else launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
     launches_++;
     EpiParams eg{};
@@ -812,9 +809,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
     pdl_suppress(big);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
-    if (sd > 1 && skip_red) {
-      normed = l + 1 < stage_l1_[stage];
-    } else if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
+    if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
       const bool last_layer = l + 1 == stage_l1_[stage];
       const bf16* gnext = !last_layer ? L_[l + 1].g1 : nullptr;
       // the stage's final residual rows are also stored straight into the
