@@ -335,10 +335,13 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
   attn_finish<HD, G>(p, seq, kh, split, n_splits, m, l, acc);
 }
 
+#ifndef TDP_ATTN_MINB
+#define TDP_ATTN_MINB 5   // resident CTAs per SM for G = 1 (MHA): 96 registers, no spills; 6 spills (measured)
+#endif
 template <int HD, int G>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, G == 1 ? TDP_ATTN_MINB : 1)
 decode_attn_kernel(DecodeAttnParams p) {
-  pdl_trigger_tail(G == 1 ? 4 : G <= 4 ? 3 : 2);   // resident CTAs per SM (registers)
+  pdl_trigger_tail(G == 1 ? TDP_ATTN_MINB : G <= 4 ? 3 : 2);   // resident CTAs per SM (registers)
   // ctx / block tables are host-uploaded metadata (complete before the
   // previous kernel ran): read before the PDL wait, which attend_range takes
   const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
