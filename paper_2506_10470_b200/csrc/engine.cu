@@ -210,6 +210,7 @@ class CudaEngine : public Engine {
   float *x_ = nullptr, *logits_ = nullptr, *part_ = nullptr;
   bf16 *a_ = nullptr, *q_ = nullptr, *ob_ = nullptr, *h_ = nullptr;
   int max_splits_cap_ = 0;
+  int64_t part_cap_ = 0;
   // arena
   int32_t* arena_ = nullptr;
   int64_t arena_cap_ = 0;
@@ -493,7 +494,11 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&h_, T * F_ * 2));
   CK(cudaMalloc(&logits_, n * V_ * 4));
   max_splits_cap_ = (int)cdiv(s_.max_seq_len, kAttnMinSplit);
-  CK(cudaMalloc(&part_, n * H_ * (int64_t)max_splits_cap_ * (hd_ + 2) * 4));
+  // (sequence x split) slots per head: every sequence at 128-token splits, or
+  // kAttnSmallN sequences at the GQA small-batch 32-token splits
+  part_cap_ = std::max<int64_t>(n * max_splits_cap_,
+                                std::min<int64_t>(n, kAttnSmallN) * cdiv(s_.max_seq_len, kAttnMinSplitGQA));
+  CK(cudaMalloc(&part_, part_cap_ * H_ * (hd_ + 2) * 4));
   cudaFree(attn_cnt_);
   CK(cudaMalloc(&attn_cnt_, n * Hkv_ * sizeof(int)));
   CK(cudaMemsetAsync(attn_cnt_, 0, n * Hkv_ * sizeof(int), st_));
@@ -737,6 +742,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       if (M.nd > 0) {
         DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, M.nd, H_, Hkv_, hd_, 0,
                             attn_cnt_};
+        dp.part_cap = part_cap_;
         plan_decode_attn(dp, mb_ctx_.data());
         if (M.nd >= nopdl_attn) pdl_suppress(true);
         launch_decode_attn(dp, st_);
@@ -762,6 +768,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     } else {
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, n, H_, Hkv_, hd_, 0,
                           attn_cnt_};
+      dp.part_cap = part_cap_;
       if (defer_qkv && qsplits > 1) {
         dp.qkv_ws = ws_;
         dp.qkv_splits = qsplits;

@@ -634,6 +634,25 @@ void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
     if (ctas * p.Hkv >= target || split <= (v2 ? 256 : kAttnMinSplit)) break;
     split >>= 1;
   }
+  // GQA at small batch: every CTA serves G query heads, so the grid is only
+  // Hkv x n x splits CTAs.  While that is below one CTA per SM, halve the
+  // split (down to 32 tokens) as long as a sequence keeps <= 8 splits (one
+  // merge round trip) and the workspace holds the partials.  Measured on
+  // Llama-2-70B heads (profiles/r1/attn_sweep_gqa8_small.txt): 1.6x at
+  // n <= 4 x 256 tokens; more splits than 8, or splitting a grid that already
+  // has >= 1 CTA per SM, was slower.
+  const int G = p.H / p.Hkv;
+  if (!v2 && G >= 4 && split == kAttnMinSplit) {
+    for (;;) {
+      int64_t ctas = 0;
+      for (int i = 0; i < p.n; ++i) ctas += (ctx[i] + split - 1) / split;
+      const int nsplit = split / 2;
+      const int64_t nsplits = (max_ctx + nsplit - 1) / nsplit;
+      if (ctas * p.Hkv >= 148 || nsplit < kAttnMinSplitGQA || nsplits > 8) break;
+      if ((int64_t)p.n * nsplits > p.part_cap) break;
+      split = nsplit;
+    }
+  }
   p.split_tokens = split;
   p.max_splits = (max_ctx + split - 1) / split;
 }

@@ -96,12 +96,19 @@ struct DecodeAttnParams {
   const float* qkv_ws = nullptr;
   int qkv_splits = 0, nqkv = 0;
   const float* rope_cs = nullptr;   // [max_pos][hd/2][2] (cos, sin)
+  int64_t part_cap = 0;  // part[] capacity in (sequence x split) slots per head (0: no GQA small splits)
 };
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 // Launch plan from the host copy of the context lengths: sets split_tokens
 // and max_splits (part[] must hold cdiv(max_seq_len, kAttnMinSplit) splits per
 // head).
 constexpr int kAttnMinSplit = 128;   // 64 measured slower (profiles/r1/optimisation_log.md)
+// GQA (G >= 4) batches too small to occupy the GPU at 128-token splits may go
+// down to 32-token splits when the workspace holds them: n * max_splits <=
+// DecodeAttnParams::part_cap (the engine sizes part[] for kAttnSmallN sequences
+// at 32-token splits)
+constexpr int kAttnMinSplitGQA = 32;
+constexpr int kAttnSmallN = 32;
 void plan_decode_attn(DecodeAttnParams& p, const int* ctx_host);
 
 // Prefill: varlen causal over each sequence's own (paged) K/V.

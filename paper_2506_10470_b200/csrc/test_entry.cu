@@ -170,7 +170,7 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
   for (int c = 0; c < copies; ++c)
     for (int i = 0; i < n; ++i)
       for (int b = 0; b < (ctx[i] + 15) / 16; ++b) bt[((size_t)c * n + i) * maxblk + b] = perm[k++];
-  const int cap = (max_ctx + kAttnMinSplit - 1) / kAttnMinSplit;
+  const int cap = (max_ctx + kAttnMinSplitGQA - 1) / kAttnMinSplitGQA;   // any launch plan fits
   bf16 *kv = nullptr, *q = nullptr, *o = nullptr;
   float* part = nullptr;
   int32_t *dctx = nullptr, *dbt = nullptr;
@@ -190,6 +190,7 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
     cudaMemcpy(dctx, ctx, n * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice);
     DecodeAttnParams p{q, kv, dctx, dbt, maxblk, o, part, 0, n, H, Hkv, hd, 0, cnt};
+    p.part_cap = (int64_t)n * cap;
     plan_decode_attn(p, ctx);
     auto run = [&](int i) {
       DecodeAttnParams pi = p;
