@@ -568,7 +568,8 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
     static const int64_t target = getenv("TDPIPE_SPLIT_TARGET") ? atoi(getenv("TDPIPE_SPLIT_TARGET")) : 288;
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, target / ctas));
+    static const int64_t smax = getenv("TDPIPE_SPLIT_MAX") ? atoi(getenv("TDPIPE_SPLIT_MAX")) : 8;   // A/B knob
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(smax, target / ctas));
     while (splits > 1 && (K / 64) / splits < 4) --splits;
     while (splits > 1 && (int64_t)splits * T * ((N + 127) / 128 * 128) > ws_cap_) --splits;
     // A/B knobs: cap the split count of the QKV GEMM (its reduce is a separate

@@ -359,3 +359,25 @@ def test_td_run_speed_of_light_accounting(tmp_path):
     assert st["alg_bytes"] == pytest.approx(want_bytes, rel=1e-9)
     assert st["alg_flops"] == pytest.approx(want_flops, rel=1e-9)
     assert 0 < st["ideal_ns"] < st["makespan_ns"]
+
+
+def test_gqa_small_batch_32_token_splits():
+    """GQA-8 decode at a batch too small to occupy the GPU (2 sequences x 1 kv
+    head): the launch plan goes down to 32-token splits, up to 8 per sequence,
+    merged in split order (kernels.h kAttnMinSplitGQA).  Context lengths hit
+    8 full splits, a ragged last split, and a single split."""
+    shape = ModelShape("gqa8_small", 1, 1024, 8, 1, 1024, 512, max_seq_len=1024)
+    W = OracleWeights(shape)
+    t = TDPipe(shape, 1, kv_blocks=256)
+    rng = np.random.default_rng(5)
+    for lengths in ([255, 200], [31, 250]):
+        prompts = [rng.integers(0, shape.vocab, size=L).astype(np.int32) for L in lengths]
+        bt = _paged([L + 2 for L in lengths])
+        out = t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * 2, lengths, bt, np.concatenate(prompts))
+        nxt = np.argmax(out, -1).astype(np.int32)
+        out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * 2, bt, nxt)
+        for i, p in enumerate(prompts):
+            ref = F.sequence_logits(W, np.concatenate([p, [nxt[i]]]))
+            _rows_ok(out[i], ref[-2])
+            _rows_ok(out2[i], ref[-1])
+    t.close()
