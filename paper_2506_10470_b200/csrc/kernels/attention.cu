@@ -101,9 +101,14 @@ __device__ __forceinline__ void attn_finish(const DecodeAttnParams& p, int seq, 
   // the last split CTA of this (sequence, kv head) merges all splits in split
   // order (deterministic) -- no separate combine launch
   __shared__ int s_last;
-  __threadfence();
+  // barrier, then one cumulative fence + ticket by thread 0 (the grid-sync
+  // pattern): the CTA's partial stores are ordered before the ticket
+  // (measured 0.5 % faster than a fence in every thread)
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[seq * p.Hkv + kh], 1) == n_splits - 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&p.counters[seq * p.Hkv + kh], 1) == n_splits - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -634,15 +639,16 @@ void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
     if (ctas * p.Hkv >= target || split <= (v2 ? 256 : kAttnMinSplit)) break;
     split >>= 1;
   }
-  // GQA at small batch: every CTA serves G query heads, so the grid is only
-  // Hkv x n x splits CTAs.  While that is below one CTA per SM, halve the
+  // Small batches: the grid is only Hkv x n x splits CTAs (GQA: few kv
+  // heads).  While that is below one CTA per SM, halve the
   // split (down to 32 tokens) as long as a sequence keeps <= 8 splits (one
   // merge round trip) and the workspace holds the partials.  Measured on
   // Llama-2-70B heads (profiles/r1/attn_sweep_gqa8_small.txt): 1.6x at
-  // n <= 4 x 256 tokens; more splits than 8, or splitting a grid that already
-  // has >= 1 CTA per SM, was slower.
+  // n <= 4 x 256 tokens (MHA, Llama-2-7B heads: 1.1-1.3x at n <= 2 x 256);
+  // more splits than 8, or splitting a grid that already has >= 1 CTA per
+  // SM, was slower.
   const int G = p.H / p.Hkv;
-  if (!v2 && G >= 4 && split == kAttnMinSplit) {
+  if (!v2 && split == kAttnMinSplit) {
     for (;;) {
       int64_t ctas = 0;
       for (int i = 0; i < p.n; ++i) ctas += (ctx[i] + split - 1) / split;

@@ -103,7 +103,7 @@ void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 // and max_splits (part[] must hold cdiv(max_seq_len, kAttnMinSplit) splits per
 // head).
 constexpr int kAttnMinSplit = 128;   // 64 measured slower (profiles/r1/optimisation_log.md)
-// GQA (G >= 4) batches too small to occupy the GPU at 128-token splits may go
+// Batches too small to occupy the GPU at 128-token splits (mostly GQA) may go
 // down to 32-token splits when the workspace holds them: n * max_splits <=
 // DecodeAttnParams::part_cap (the engine sizes part[] for kAttnSmallN sequences
 // at 32-token splits)
