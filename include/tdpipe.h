@@ -11,7 +11,8 @@
  *
  * Conventions
  *  - Every call returns td_status (0 = TD_OK, < 0 = error); no C++ exception
- *    crosses the ABI.  On error, td_last_error(ctx) holds a message.
+ *    crosses the ABI.  On error, td_last_error(ctx) holds a message; a failed
+ *    td_create leaves its message in td_last_error(NULL) (per thread).
  *  - All pointers in signatures are HOST pointers unless stated otherwise;
  *    the library copies what it needs (caller keeps ownership).
  *  - A td_ctx must not be used by two caller threads at once.
@@ -90,8 +91,7 @@ typedef struct td_model_shape {
 
 typedef struct td_options {
   int32_t executor;             /* TD_EXEC_CUDA | TD_EXEC_NULL                         */
-  int32_t device;               /* CUDA device of stage 0 (single-process mode)        */
-  int32_t devices_per_stage;    /* 0: all stages on `device`; 1: stage s on device+s   */
+  int32_t device;               /* CUDA device of this process (every stage it runs)   */
   int32_t block_size;           /* KV block (page) size in tokens, B (default 16)      */
   int64_t kv_blocks;            /* C; 0 = fill HBM (min over stages)                   */
   double hbm_reserve_frac;      /* HBM kept free when kv_blocks = 0 (default 0.06)     */
@@ -179,6 +179,9 @@ void td_default_options(td_options* o);
 td_status td_create(const td_model_shape* shape, int32_t n_stages, const td_options* opts,
                     struct td_ctx** out);
 void td_destroy(struct td_ctx* ctx);
+/* Message of the last error on `ctx`; ctx == NULL: the message of the last
+ * failed td_create on the calling thread ("" if none).  The pointer stays
+ * valid until the next call on the same ctx (or thread, for NULL). */
 const char* td_last_error(const struct td_ctx* ctx);
 
 /* Submit one request (offline request set).  The prompt is
@@ -202,8 +205,11 @@ td_status td_run(struct td_ctx* ctx, td_run_stats* st);
  * *n = number of tokens.  TD_ERANGE if cap < *n (n still set). */
 td_status td_get_output(struct td_ctx* ctx, int64_t id, int32_t* buf, int32_t cap, int32_t* n);
 
-/* All outputs at once: out[id * stride + j] for j < n_out[id]; one D2H copy. */
-td_status td_get_outputs(struct td_ctx* ctx, int32_t* out, int32_t stride, int32_t* n_out);
+/* All outputs at once (one D2H copy): out[id * stride + j] for j < n_out[id],
+ * id < number of submitted requests.  `out` holds n_rows * stride int32 and
+ * `n_out` n_rows int32, both caller-owned.  TD_ERANGE (nothing written) if
+ * n_rows < the number of submitted requests or stride < the longest output. */
+td_status td_get_outputs(struct td_ctx* ctx, int32_t* out, int32_t n_rows, int32_t stride, int32_t* n_out);
 
 /* fp32 logits [n_steps, vocab] of request `id` (requires record_logits). */
 td_status td_get_logits(struct td_ctx* ctx, int64_t id, float* buf, int64_t cap, int32_t* n_steps);
@@ -288,6 +294,20 @@ td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t
  * the engine's plan.  K/V, q are zeros (timing only). */
 td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx, int32_t H, int32_t Hkv, int32_t hd,
                         int32_t iters, float* us_per_call);
+
+/* Weight read-back (testing only): the bf16 bit patterns of F9 tensor
+ * `tensor_id` (SURVEY.md §8(c) F9 enumeration: 0 = embedding [V, d]; layer l:
+ * 1+9l+{0 g1 [d], 1 Wq [H hd, d], 2 Wk [Hkv hd, d], 3 Wv [Hkv hd, d],
+ * 4 Wo [d, H hd], 5 g2 [d], 6 Wg [F, d], 7 Wu [F, d], 8 Wd [d, F]};
+ * 1+9L = final norm [d]; 2+9L = LM head [V, d]) in its LOGICAL row-major
+ * [rows, cols] layout, undoing the device's tile packing and the RoPE-pair /
+ * gate-up row interleaving.  Copies min(cap, rows*cols) elements into `out`
+ * (caller-owned); *rows / *cols are always set.  TD_EINVAL if the tensor is
+ * not held by this process (another rank's stage), TD_ERANGE if cap is too
+ * small.  Lets a test check the device weights bit for bit against the
+ * oracle's independent implementation of the recipe. */
+td_status td_get_weight(struct td_ctx* ctx, int32_t tensor_id, uint16_t* out, int64_t cap, int64_t* rows,
+                        int64_t* cols);
 
 /* Generate the two ncclUniqueIds (256 bytes) rank 0 shares with all ranks. */
 td_status td_nccl_ids(void* out256);

@@ -40,6 +40,13 @@ struct td_ctx {
   std::vector<std::pair<int64_t, int64_t>> kv_samples;
 };
 
+static thread_local std::string g_create_err;   // td_last_error(NULL)
+
+static td_status create_fail(td_status st, const std::string& m) {
+  g_create_err = m;
+  return st;
+}
+
 static td_status fail(td_ctx* c, td_status st, const std::string& m) {
   if (c) c->err = m;
   return st;
@@ -49,7 +56,6 @@ extern "C" void td_default_options(td_options* o) {
   std::memset(o, 0, sizeof *o);
   o->executor = TD_EXEC_CUDA;
   o->device = 0;
-  o->devices_per_stage = 0;
   o->block_size = 16;
   o->kv_blocks = 0;
   o->hbm_reserve_frac = 0.06;
@@ -112,24 +118,32 @@ extern "C" td_status td_create(const td_model_shape* s, int32_t n_stages, const 
   if (c->opt.profile_csv) c->profile_path = c->opt.profile_csv;
   c->opt.profile_csv = nullptr;
   const auto& m = c->shape;
-  if (n_stages < 1 || n_stages > m.n_layers) return TD_EINVAL;
-  if (m.n_heads <= 0 || m.n_kv_heads <= 0 || m.n_heads % m.n_kv_heads) return TD_EINVAL;
-  if (m.d_model <= 0 || m.d_model % m.n_heads) return TD_EINVAL;
+  g_create_err.clear();
+  if (n_stages < 1 || n_stages > m.n_layers) return create_fail(TD_EINVAL, "n_stages must be in [1, n_layers]");
+  if (m.n_heads <= 0 || m.n_kv_heads <= 0 || m.n_heads % m.n_kv_heads)
+    return create_fail(TD_EINVAL, "n_kv_heads must divide n_heads");
+  if (m.d_model <= 0 || m.d_model % m.n_heads) return create_fail(TD_EINVAL, "n_heads must divide d_model");
   const int hd = m.d_model / m.n_heads;
-  if (hd != 16 && hd != 32 && hd != 64 && hd != 128) return TD_EINVAL;
-  if (m.d_model % 64 || m.d_ffn % 64 || m.d_ffn <= 0 || m.vocab <= 0 || m.max_seq_len <= 0) return TD_EINVAL;
-  if (c->opt.block_size < 1) return TD_EINVAL;
-  if (c->opt.executor != TD_EXEC_NULL && c->opt.block_size != 16) return TD_EINVAL;  // kernels use 16-token pages
-  if (c->opt.prefill_token_budget < 1 || c->opt.max_batch_seqs < 1 || c->opt.fp_stride < 1) return TD_EINVAL;
-  if (c->opt.world_size < 1 || c->opt.rank < 0 || c->opt.rank >= c->opt.world_size) return TD_EINVAL;
-  if (c->opt.world_size > 1 && c->opt.world_size != n_stages) return TD_EINVAL;
-  if (c->opt.handoff != TD_HANDOFF_PEER && c->opt.handoff != TD_HANDOFF_NCCL) return TD_EINVAL;
+  if (hd != 16 && hd != 32 && hd != 64 && hd != 128) return create_fail(TD_EINVAL, "head_dim must be 16/32/64/128");
+  if (m.d_model % 64 || m.d_ffn % 64 || m.d_ffn <= 0 || m.vocab <= 0 || m.max_seq_len <= 0)
+    return create_fail(TD_EINVAL, "d_model and d_ffn must be multiples of 64; vocab, max_seq_len > 0");
+  if (c->opt.block_size < 1) return create_fail(TD_EINVAL, "block_size < 1");
+  if (c->opt.executor != TD_EXEC_NULL && c->opt.block_size != 16)
+    return create_fail(TD_EINVAL, "the CUDA executor uses 16-token KV pages (block_size 16)");
+  if (c->opt.prefill_token_budget < 1 || c->opt.max_batch_seqs < 1 || c->opt.fp_stride < 1)
+    return create_fail(TD_EINVAL, "prefill_token_budget, max_batch_seqs and fp_stride must be >= 1");
+  if (c->opt.world_size < 1 || c->opt.rank < 0 || c->opt.rank >= c->opt.world_size)
+    return create_fail(TD_EINVAL, "rank must be in [0, world_size)");
+  if (c->opt.world_size > 1 && c->opt.world_size != n_stages)
+    return create_fail(TD_EINVAL, "world_size > 1 needs world_size == n_stages (one stage per process)");
+  if (c->opt.handoff != TD_HANDOFF_PEER && c->opt.handoff != TD_HANDOFF_NCCL)
+    return create_fail(TD_EINVAL, "unknown handoff");
   if (c->opt.executor != TD_EXEC_NULL && c->opt.world_size > 1 && c->opt.handoff == TD_HANDOFF_PEER &&
       !c->opt.allgather)
-    return TD_EINVAL;
+    return create_fail(TD_EINVAL, "TD_HANDOFF_PEER needs the allgather callback");
   if (!c->profile_path.empty()) {
     std::string e;
-    if (!read_profile(c->profile_path, &c->tdec, &c->tpre, &e)) return TD_EINVAL;
+    if (!read_profile(c->profile_path, &c->tdec, &c->tpre, &e)) return create_fail(TD_EINVAL, e);
   }
   if (c->opt.executor == TD_EXEC_NULL) {
     c->kv_blocks = c->opt.kv_blocks > 0 ? c->opt.kv_blocks : (int64_t)1 << 30;
@@ -137,10 +151,7 @@ extern "C" td_status td_create(const td_model_shape* s, int32_t n_stages, const 
     Engine* e = nullptr;
     std::string err;
     td_status st = Engine::create(c->shape, n_stages, c->opt, &e, &err);
-    if (st != TD_OK) {
-      fprintf(stderr, "td_create: %s\n", err.c_str());
-      return st;
-    }
+    if (st != TD_OK) return create_fail(st, err);
     c->engine.reset(e);
     c->kv_blocks = e->kv_blocks();
   }
@@ -150,7 +161,7 @@ extern "C" td_status td_create(const td_model_shape* s, int32_t n_stages, const 
 
 extern "C" void td_destroy(td_ctx* c) { delete c; }
 
-extern "C" const char* td_last_error(const td_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+extern "C" const char* td_last_error(const td_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 extern "C" int64_t td_submit(td_ctx* c, const int32_t* prompt, int32_t n_prompt, int32_t predicted_len,
                              int32_t max_new_tokens) {
@@ -421,12 +432,15 @@ extern "C" td_status td_get_output(td_ctx* c, int64_t id, int32_t* buf, int32_t 
   return TD_OK;
 }
 
-extern "C" td_status td_get_outputs(td_ctx* c, int32_t* out, int32_t stride, int32_t* n_out) {
-  if (!c || !out || !n_out) return TD_EINVAL;
+extern "C" td_status td_get_outputs(td_ctx* c, int32_t* out, int32_t n_rows, int32_t stride, int32_t* n_out) {
+  if (!c || !out || !n_out || stride < 0) return TD_EINVAL;
   if (td_status st = cache_outputs(c)) return st;
+  if ((size_t)std::max(n_rows, 0) < c->outputs.size())
+    return fail(c, TD_ERANGE, "n_rows < number of submitted requests");
+  for (const auto& o : c->outputs)
+    if ((int32_t)o.size() > stride) return fail(c, TD_ERANGE, "stride < longest output");
   for (size_t i = 0; i < c->outputs.size(); ++i) {
     const auto& o = c->outputs[i];
-    if ((int32_t)o.size() > stride) return TD_ERANGE;
     n_out[i] = (int32_t)o.size();
     if (!o.empty()) std::memcpy(out + i * (size_t)stride, o.data(), o.size() * sizeof(int32_t));
   }
@@ -531,6 +545,21 @@ extern "C" td_status td_get_timing(td_ctx* c, const char* name, int64_t* launche
   if (total_ms) *total_ms = t.ms;
   if (bytes) *bytes = t.bytes;
   if (flops) *flops = t.flops;
+  return TD_OK;
+}
+
+extern "C" td_status td_get_weight(td_ctx* c, int32_t tensor_id, uint16_t* out, int64_t cap, int64_t* rows,
+                                   int64_t* cols) {
+  if (!c || !rows || !cols) return TD_EINVAL;
+  if (!c->engine) return fail(c, TD_ESTATE, "null executor");
+  std::vector<uint16_t> w;
+  int64_t r = 0, k = 0;
+  if (td_status st = c->engine->get_weight(tensor_id, &w, &r, &k)) return fail(c, st, c->engine->error);
+  *rows = r;
+  *cols = k;
+  if (!out) return TD_OK;
+  if (cap < r * k) return fail(c, TD_ERANGE, "cap < rows * cols");
+  std::memcpy(out, w.data(), (size_t)(r * k) * sizeof(uint16_t));
   return TD_OK;
 }
 

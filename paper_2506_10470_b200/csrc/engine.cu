@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -131,6 +132,7 @@ class CudaEngine : public Engine {
     timing_ = on;
   }
   bool get_timing(const std::string& name, KernelTiming* t) override;
+  td_status get_weight(int tid, std::vector<uint16_t>* out, int64_t* rows, int64_t* cols) override;
 
  private:
   void release();
@@ -1179,6 +1181,73 @@ td_status CudaEngine::get_logits(int64_t rid, std::vector<float>* out, int* n_st
 td_status CudaEngine::kv_reset() {
   CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * (own_l1_ - own_l0_), st_));
   CK(cudaStreamSynchronize(st_));
+  return TD_OK;
+}
+
+// ------------------------------------------------------- weight read-back
+// td_get_weight: copy the physical tensor D2H and undo the device layout on the
+// host -- tile packing (pack_offset), the rotate-half pair interleave of the q
+// and k rows ((i, i+hd/2) stored as rows (2i, 2i+1)) and the gate/up row
+// interleave (gate j = row 2j, up j = row 2j+1).
+td_status CudaEngine::get_weight(int tid, std::vector<uint16_t>* out, int64_t* rows, int64_t* cols) {
+  CK(cudaSetDevice(dev_));
+  const int L = s_.n_layers;
+  const int64_t nqkv = (int64_t)(H_ + 2 * Hkv_) * hd_;
+  const bf16* src = nullptr;
+  int64_t phys_elems = 0, K = 0;
+  bool packed = false;
+  std::function<int64_t(int64_t)> prow = [](int64_t r) { return r; };   // logical row -> physical row
+  auto pad = [](int64_t r) { return (r + 127) / 128 * 128; };
+  auto rope_row = [this](int64_t base, int64_t r) {
+    const int64_t h = r / hd_, i = r % hd_;
+    const int64_t j = i < hd_ / 2 ? 2 * i : 2 * (i - hd_ / 2) + 1;
+    return base + h * hd_ + j;
+  };
+  if (tid == 0) {
+    if (!E_) { error = "embedding not held by this process"; return TD_EINVAL; }
+    src = E_; *rows = V_; *cols = d_; phys_elems = (int64_t)V_ * d_;
+  } else if (tid == 1 + 9 * L) {
+    if (!gf_) { error = "final norm not held by this process"; return TD_EINVAL; }
+    src = gf_; *rows = 1; *cols = d_; phys_elems = d_;
+  } else if (tid == 2 + 9 * L) {
+    if (!Wlm_) { error = "LM head not held by this process"; return TD_EINVAL; }
+    src = Wlm_; *rows = V_; *cols = d_; K = d_; packed = true; phys_elems = pad(V_) * d_;
+  } else if (tid >= 1 && tid < 1 + 9 * L) {
+    const int l = (tid - 1) / 9, which = (tid - 1) % 9;
+    if (l < own_l0_ || l >= own_l1_) { error = "layer not held by this process"; return TD_EINVAL; }
+    const LayerW& w = L_[l];
+    switch (which) {
+      case 0: src = w.g1; *rows = 1; *cols = d_; phys_elems = d_; break;
+      case 5: src = w.g2; *rows = 1; *cols = d_; phys_elems = d_; break;
+      case 1: case 2: case 3: {
+        src = w.wqkv; K = d_; packed = true; phys_elems = pad(nqkv) * d_;
+        *cols = d_;
+        *rows = which == 1 ? (int64_t)H_ * hd_ : (int64_t)Hkv_ * hd_;
+        if (which == 1) prow = [=](int64_t r) { return rope_row(0, r); };
+        else if (which == 2) prow = [=](int64_t r) { return rope_row((int64_t)H_ * hd_, r); };
+        else prow = [=](int64_t r) { return (int64_t)(H_ + Hkv_) * hd_ + r; };
+        break;
+      }
+      case 4: src = w.wo; K = (int64_t)H_ * hd_; packed = true; phys_elems = pad(d_) * K; *rows = d_; *cols = K; break;
+      case 6: case 7:
+        src = w.wgu; K = d_; packed = true; phys_elems = pad(2LL * F_) * d_; *rows = F_; *cols = d_;
+        prow = [=](int64_t r) { return 2 * r + (which == 7 ? 1 : 0); };
+        break;
+      case 8: src = w.wd; K = F_; packed = true; phys_elems = pad(d_) * F_; *rows = d_; *cols = F_; break;
+    }
+  } else {
+    error = "tensor id out of range";
+    return TD_EINVAL;
+  }
+  std::vector<uint16_t> phys((size_t)phys_elems);
+  CK(cudaStreamSynchronize(st_));
+  CK(cudaMemcpy(phys.data(), src, (size_t)phys_elems * 2, cudaMemcpyDeviceToHost));
+  out->assign((size_t)(*rows * *cols), 0);
+  for (int64_t r = 0; r < *rows; ++r) {
+    const int64_t p = prow(r);
+    for (int64_t c = 0; c < *cols; ++c)
+      (*out)[(size_t)(r * *cols + c)] = phys[(size_t)(packed ? pack_offset(p, c, K) : p * *cols + c)];
+  }
   return TD_OK;
 }
 

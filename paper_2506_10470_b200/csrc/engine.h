@@ -48,6 +48,8 @@ class Engine : public ExecHooks {
   virtual td_status kv_reset() = 0;
   virtual td_status profile(int b_max, int k_max, int ctx_len, std::vector<int64_t>* tdec,
                             std::vector<int64_t>* tpre) = 0;
+  // logical [rows, cols] bf16 bits of F9 tensor `tid` (td_get_weight)
+  virtual td_status get_weight(int tid, std::vector<uint16_t>* out, int64_t* rows, int64_t* cols) = 0;
   virtual void set_timing(bool on) = 0;
   virtual bool get_timing(const std::string& name, KernelTiming* t) = 0;
   std::string error;

@@ -32,7 +32,7 @@ class td_model_shape(C.Structure):
 
 
 class td_options(C.Structure):
-    _fields_ = [("executor", C.c_int32), ("device", C.c_int32), ("devices_per_stage", C.c_int32),
+    _fields_ = [("executor", C.c_int32), ("device", C.c_int32),
                 ("block_size", C.c_int32), ("kv_blocks", C.c_int64), ("hbm_reserve_frac", C.c_double),
                 ("prefill_token_budget", C.c_int32), ("max_batch_seqs", C.c_int32),
                 ("fp_stride", C.c_int32), ("fp_horizon", C.c_int32), ("policy", C.c_int32),
@@ -70,7 +70,8 @@ class td_batch(C.Structure):
 EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td_submit", "td_upload",
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
-           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace"]
+           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace",
+           "td_get_weight"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -90,7 +91,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_upload.argtypes = [C.c_void_p]
     lib.td_run.argtypes = [C.c_void_p, P(td_run_stats)]
     lib.td_get_output.argtypes = [C.c_void_p, C.c_int64, P(C.c_int32), C.c_int32, P(C.c_int32)]
-    lib.td_get_outputs.argtypes = [C.c_void_p, P(C.c_int32), C.c_int32, P(C.c_int32)]
+    lib.td_get_outputs.argtypes = [C.c_void_p, P(C.c_int32), C.c_int32, C.c_int32, P(C.c_int32)]
+    lib.td_get_weight.argtypes = [C.c_void_p, C.c_int32, P(C.c_uint16), C.c_int64, P(C.c_int64), P(C.c_int64)]
     lib.td_get_logits.argtypes = [C.c_void_p, C.c_int64, P(C.c_float), C.c_int64, P(C.c_int32)]
     lib.td_reset.argtypes = [C.c_void_p]
     lib.td_stage_forward.argtypes = [C.c_void_p, C.c_int32, P(td_batch), C.c_void_p, C.c_void_p]
@@ -183,7 +185,7 @@ class TDPipe:
         self.ctx = C.c_void_p()
         st = lib().td_create(C.byref(make_shape(shape)), int(n_stages), C.byref(o), C.byref(self.ctx))
         if st != TD_OK:
-            raise TDError(f"td_create failed: {st}")
+            raise TDError(f"td_create failed ({st}): {lib().td_last_error(None).decode()}")
         self.n_stages = n_stages
 
     def close(self):
@@ -239,9 +241,18 @@ class TDPipe:
     def td_get_outputs(self, n_requests: int, stride: int):
         out = np.zeros((n_requests, stride), dtype=np.int32)
         n = np.zeros(n_requests, dtype=np.int32)
-        self._check(lib().td_get_outputs(self.ctx, _ptr(out, C.c_int32), stride, _ptr(n, C.c_int32)),
+        self._check(lib().td_get_outputs(self.ctx, _ptr(out, C.c_int32), n_requests, stride, _ptr(n, C.c_int32)),
                     "td_get_outputs")
         return out, n
+
+    def td_get_weight(self, tensor_id: int) -> np.ndarray:
+        """bf16 bit patterns (uint16) of F9 tensor `tensor_id`, logical [rows, cols]."""
+        r, c = C.c_int64(), C.c_int64()
+        lib().td_get_weight(self.ctx, int(tensor_id), None, 0, C.byref(r), C.byref(c))
+        buf = np.zeros(max(r.value * c.value, 1), dtype=np.uint16)
+        self._check(lib().td_get_weight(self.ctx, int(tensor_id), _ptr(buf, C.c_uint16), buf.size, C.byref(r),
+                                        C.byref(c)), "td_get_weight")
+        return buf[: r.value * c.value].reshape(r.value, c.value)
 
     def td_get_logits(self, rid: int) -> np.ndarray:
         ns = C.c_int32(0)

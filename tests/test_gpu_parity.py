@@ -245,35 +245,98 @@ def test_td_run_pphb_chunked_prefill_teacher_forced(tmp_path):
     assert n_chunk > 0 and "H" in kinds
 
 
+def _prefill_in_budget(t, prompts, bt, budget=2048):
+    """Prefill every prompt through td_stage_forward in <= budget-token
+    micro-batches (the controller's prefill budget); returns the
+    last-position logits of every sequence."""
+    outs, i = [], 0
+    while i < len(prompts):
+        j, tok = i, 0
+        while j < len(prompts) and (j == i or tok + len(prompts[j]) <= budget):
+            tok += len(prompts[j])
+            j += 1
+        L = [len(p) for p in prompts[i:j]]
+        outs.append(t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * len(L), L, bt[i:j], np.concatenate(prompts[i:j])))
+        i = j
+    return np.concatenate(outs)
+
+
+def _check_sequences(W, prompts, nxt, out, out2, idx):
+    for i in idx:
+        ref = F.sequence_logits(W, np.concatenate([prompts[i], [nxt[i]]]))
+        _rows_ok(out[i], ref[-2])
+        _argmax_ok(out[i], ref[-2])
+        _rows_ok(out2[i], ref[-1])
+
+
 @pytest.mark.slow
 def test_llama7b_shaped_bench_launch_config():
     """Full-size Llama-2-7B layers (d 4096, F 11008, V 32000) at the bench's
-    launch configuration: a 2048-token ShareGPT-mix prefill micro-batch, then a
-    decode step of all its sequences.  2 of the 32 layers ("the
-    model is composed of layers with the same structure, so reducing the number
-    of layers does not affect its computational ... characteristics");
-    sampled sequences checked one by one against the oracle."""
+    launch configuration: the C2 request set (256 ShareGPT-length prompts,
+    seed 2) prefilled in <= 2048-token micro-batches, then ONE decode
+    micro-batch of all 256 sequences -- the b > 128 path the bench takes
+    (token-major tcgen05 kernel for the wide QKV / gate-up / LM-head GEMMs,
+    n >= 129 attention plan, split-K O / down) -- and a second decode step
+    (the fused QKV-reduce attention prologue).  2 of the 32 layers
+    (the layers share one structure).  Checked against the fp64
+    oracle one by one: the 8 shortest, the 8 longest (multi-split attention)
+    and 8 random sequences."""
     shape = SHAPES["llama2_7b"].with_layers(2)
-    wl = generate_workload(64, shape.vocab, 2)
-    lengths, prompts = [], []
-    for r in wl.requests:
-        if sum(lengths) + len(r.prompt) > 2048:
-            break
-        lengths.append(len(r.prompt))
-        prompts.append(r.prompt)
-    t = TDPipe(shape, 1, kv_blocks=2048)
-    bt = _paged([L + 2 for L in lengths])
-    out = t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * len(lengths), lengths, bt, np.concatenate(prompts))
+    wl = generate_workload(256, shape.vocab, 2)
+    prompts = [r.prompt for r in wl.requests]
+    lengths = [len(p) for p in prompts]
+    t = TDPipe(shape, 1, kv_blocks=8192)
+    bt = _paged([L + 3 for L in lengths])
+    out = _prefill_in_budget(t, prompts, bt)
     nxt = np.argmax(out, -1).astype(np.int32)
-    out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * len(lengths), bt, nxt)
+    out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * 256, bt, nxt)
+    nxt2 = np.argmax(out2, -1).astype(np.int32)
+    out3 = t.td_stage_forward(0, TD_BATCH_DECODE, [L + 1 for L in lengths], [1] * 256, bt, nxt2)
     t.close()
     W = OracleWeights(shape)
-    sample = sorted(range(len(lengths)), key=lambda i: lengths[i])[:3]
-    for i in sample:
-        seq = np.concatenate([prompts[i], [nxt[i]]])
-        ref = F.sequence_logits(W, seq)
-        _rows_ok(out[i], ref[-2])
-        _rows_ok(out2[i], ref[-1])
+    order = sorted(range(256), key=lambda i: lengths[i])
+    rng = np.random.default_rng(0)
+    idx = sorted(set(order[:8] + order[-8:] + list(rng.choice(256, 8, replace=False))))
+    _check_sequences(W, prompts, nxt, out, out2, idx)
+    for i in order[-4:]:   # the second decode step of the longest sequences
+        ref = F.sequence_logits(W, np.concatenate([prompts[i], [nxt[i], nxt2[i]]]))
+        _rows_ok(out3[i], ref[-1])
+
+
+@pytest.mark.slow
+def test_llama7b_split_k_decode_tolerance():
+    """Decode micro-batches of 1, 8 and 40 sequences at Llama-2-7B width, where
+    the decode GEMMs split K (8 / 8 / 4 splits on QKV, O, gate-up, down) and
+    attention splits the context: every sequence's logits vs the fp64 oracle,
+    and the same sequence decoded in different batch compositions agrees
+    within the tolerance (split counts change rounding, never the result)."""
+    shape = SHAPES["llama2_7b"].with_layers(2)
+    wl = generate_workload(48, shape.vocab, 21)
+    prompts = [r.prompt for r in wl.requests][:40]
+    lengths = [len(p) for p in prompts]
+    W = OracleWeights(shape)
+    res = {}
+    for b in (1, 8, 40):
+        t = TDPipe(shape, 1, kv_blocks=4096)
+        bt = _paged([L + 2 for L in lengths[:b]])
+        out = _prefill_in_budget(t, prompts[:b], bt)
+        nxt = np.argmax(out, -1).astype(np.int32)
+        out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths[:b], [1] * b, bt, nxt)
+        t.close()
+        res[b] = (nxt, out2)
+    refs = {}
+    for b, (nxt, out2) in res.items():
+        for i in range(b):
+            key = (i, int(nxt[i]))
+            if key not in refs:
+                refs[key] = F.sequence_logits(W, np.concatenate([prompts[i], [nxt[i]]]))[-1]
+            _rows_ok(out2[i], refs[key])
+    # batch composition: the same sequence decoded among 1 / 8 / 40 sequences
+    for i in range(8):
+        if res[8][0][i] == res[40][0][i]:
+            assert F.max_abs_rel(res[8][1][i], res[40][1][i]).max() <= TOL
+    if res[1][0][0] == res[8][0][0]:
+        assert F.max_abs_rel(res[1][1][0], res[8][1][0]).max() <= TOL
 
 
 @pytest.mark.slow
@@ -281,9 +344,9 @@ def test_llama70b_shaped_layer_gqa8():
     """C5 shape (Llama-2-70B: d 8192, H 64 / Hkv 8, F 28672, V 32000), one of
     its 80 layers: a <= 2048-token ShareGPT-mix prefill micro-batch and a decode
     step of all its sequences, i.e. the GQA-8 decode-attention kernel and the
-    wide decode / prefill GEMMs at full width; the shortest sequence is checked
-    against the fp64 oracle (generating this layer's weights in fp64 takes the
-    oracle ~1 min)."""
+    wide decode / prefill GEMMs at full width.  EVERY sequence is checked
+    against the fp64 oracle (prefill and decode logits), including the long
+    multi-split ones."""
     shape = SHAPES["llama2_70b"].with_layers(1)
     wl = generate_workload(64, shape.vocab, 5)
     lengths, prompts = [], []
@@ -298,11 +361,59 @@ def test_llama70b_shaped_layer_gqa8():
     nxt = np.argmax(out, -1).astype(np.int32)
     out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * len(lengths), bt, nxt)
     t.close()
-    W = OracleWeights(shape)
-    for i in sorted(range(len(lengths)), key=lambda i: lengths[i])[:1]:
-        ref = F.sequence_logits(W, np.concatenate([prompts[i], [nxt[i]]]))
-        _rows_ok(out[i], ref[-2])
-        _rows_ok(out2[i], ref[-1])
+    assert max(lengths) > 256   # at least one multi-split decode-attention sequence
+    _check_sequences(OracleWeights(shape), prompts, nxt, out, out2, range(len(lengths)))
+
+
+@pytest.mark.slow
+def test_llama70b_shaped_layer_gqa8_large_decode_batch():
+    """GQA-8 at the C5 stage's decode batch sizes: 128 ShareGPT-length
+    sequences (several prefill micro-batches) decoded in ONE micro-batch at
+    Llama-2-70B width (tensor-bound decode GEMMs, GQA decode attention over
+    many CTAs); sampled sequences (4 shortest, 4 longest, 4 random) vs the fp64
+    oracle."""
+    shape = SHAPES["llama2_70b"].with_layers(1)
+    wl = generate_workload(128, shape.vocab, 55)
+    prompts = [r.prompt for r in wl.requests]
+    lengths = [len(p) for p in prompts]
+    t = TDPipe(shape, 1, kv_blocks=4096)
+    bt = _paged([L + 2 for L in lengths])
+    out = _prefill_in_budget(t, prompts, bt)
+    nxt = np.argmax(out, -1).astype(np.int32)
+    out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * 128, bt, nxt)
+    t.close()
+    order = sorted(range(128), key=lambda i: lengths[i])
+    rng = np.random.default_rng(1)
+    idx = sorted(set(order[:4] + order[-4:] + list(rng.choice(128, 4, replace=False))))
+    _check_sequences(OracleWeights(shape), prompts, nxt, out, out2, idx)
+
+
+def test_device_weights_bit_identical_to_oracle_recipe():
+    """F9: the device and the oracle implement the
+    counter-based weight recipe independently; every tensor of the tiny model
+    (and a GQA variant) read back through td_get_weight (logical layout) must
+    equal oracle/weights.py bit for bit -- compared by SHA-256 of the bf16 bits
+    and elementwise."""
+    import hashlib
+    from oracle import weights as Wt
+    for shape, stages in ((SHAPES["tiny"], 1), (SHAPES["tiny_gqa"].with_layers(3), 2)):
+        W = OracleWeights(shape)
+        t = TDPipe(shape, stages, kv_blocks=16)
+        L = shape.n_layers
+        names = ["g1", "wq", "wk", "wv", "wo", "g2", "wg", "wu", "wd"]
+        want = {0: W.embed(), 1 + 9 * L: W.final_norm()[None, :], 2 + 9 * L: W.lm_head()}
+        for l in range(L):
+            for j, nm in enumerate(names):
+                v = W.layer(l)[nm]
+                want[1 + 9 * l + j] = v[None, :] if v.ndim == 1 else v
+        for tid, ref in want.items():
+            ref_bits = (np.ascontiguousarray(ref, np.float32).view(np.uint32) >> 16).astype(np.uint16)
+            got = t.td_get_weight(tid)
+            assert got.shape == ref_bits.shape, tid
+            assert hashlib.sha256(got.tobytes()).hexdigest() == hashlib.sha256(ref_bits.tobytes()).hexdigest(), tid
+            assert np.array_equal(got, ref_bits), tid
+        t.close()
+        assert Wt.tensor_id(0, "lm", L) == 2 + 9 * L
 
 
 def test_decode_attention_long_context_many_pages():
