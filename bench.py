@@ -93,35 +93,12 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- oracle arm
+# SURVEY.md §8(d) "Oracle timing": the oracle as it stands (oracle/, numpy fp32
+# as §8(d) states, BLAS threads = the cores this process may use), timed on
+# the GPU box's host in the same harness run: C1 end to end; a C2 slice (one
+# 2,048-token prefill + 8 decode steps at b = 256); reference-scheduler
+# decisions/s on the C5 request set.  A baseline, not the target.
 _ORACLE_W = {}
-
-
-def oracle_sample(shape_name="llama2_7b", layers=2, n_tokens=48):
-    """The oracle as it stands, on a bounded sample of the C2 workload: greedy
-    decode of `n_tokens` tokens of request 0 through `layers` of the 32 layers,
-    scaled to the full depth.  Weight generation is setup (cached, untimed).
-    Returns (tokens/s, seconds, description)."""
-    from oracle import forward as F
-    from oracle.weights import OracleWeights
-    full = SHAPES[shape_name]
-    shape = full.with_layers(layers)
-    wl = config_workload("C2")
-    prompt = wl.requests[0].prompt
-    key = (shape_name, layers)
-    if key not in _ORACLE_W:
-        W = OracleWeights(shape)
-        W.embed(); W.lm_head(); W.final_norm()
-        for l in range(layers):
-            W.layer(l)
-        _ORACLE_W[key] = W
-    W = _ORACLE_W[key]
-    t0 = time.perf_counter()
-    F.greedy_generate(W, prompt, n_tokens)
-    dt = time.perf_counter() - t0
-    scaled = dt * full.n_layers / layers
-    desc = (f"oracle greedy decode of {n_tokens} tokens of C2 request 0 (prompt {len(prompt)}) through "
-            f"{layers}/{full.n_layers} Llama-2-7B-shaped layers, fp64 numpy, time scaled x{full.n_layers / layers:g}")
-    return n_tokens / scaled, dt, desc
 
 
 def cpu_cores():
@@ -131,23 +108,181 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def host_info():
+    """cores used, cpu_count, CPU model, BLAS vendor/threads (threadpoolctl)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        import threadpoolctl
+        for d in threadpoolctl.threadpool_info():
+            if d.get("user_api") == "blas":
+                blas = {"vendor": d.get("internal_api"), "version": d.get("version"),
+                        "threads": d.get("num_threads"), "arch": d.get("architecture")}
+                break
+    except Exception:
+        pass
+    return {"cores": cpu_cores(), "cpu_count": os.cpu_count(), "cpu_model": model, "blas": blas}
+
+
+def _blas_threads():
+    try:
+        import threadpoolctl
+        return threadpoolctl.threadpool_limits(limits=cpu_cores(), user_api="blas")
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def oracle_c1():
+    """C1 end to end: the 8 C1 requests (prompt 16 / output 16), greedy decode
+    per request with the F6 KV cache (oracle/cached.py), tiny model, fp32."""
+    from oracle import cached as Cc
+    from oracle.weights import OracleWeights
+    wl = config_workload("C1")
+    W = OracleWeights(SHAPES["tiny"])
+    Cc.greedy_generate_cached(W, wl.requests[0].prompt, 2, dtype=np.float32)   # weights + casts: setup
+    t0 = time.perf_counter()
+    gen = 0
+    for r in wl.requests:
+        toks, _ = Cc.greedy_generate_cached(W, r.prompt, r.max_new_tokens, dtype=np.float32)
+        gen += len(toks)
+    dt = time.perf_counter() - t0
+    return {"value": gen / dt, "unit": UNIT, "seconds": round(dt, 3), "generated": gen,
+            "sample": "C1 end to end: 8 requests x (prompt 16, output 16), tiny model, fp32, per-request KV cache"}
+
+
+def oracle_c2_slice(layers=2, n_dec=8, b=256):
+    """C2 slice: one <= 2,048-token prefill micro-batch of
+    C2 prompts, then `n_dec` decode steps of b = 256 C2 requests, through
+    `layers` of the 32 Llama-2-7B layers and the LM head, numpy fp32 with the
+    F6 per-request KV cache; the per-layer time (measured minus a 0-layer run)
+    is scaled to 32 layers.  The decode requests' caches hold seeded random
+    K/V at their C2 prompt lengths (their 58k-token prefill is not part of the
+    slice).  Returns generated tokens/s (the bench metric) of the slice."""
+    from oracle import cached as Cc
+    from oracle.weights import OracleWeights
+    full = SHAPES["llama2_7b"]
+    shape = full.with_layers(layers)
+    key = ("c2", layers)
+    if key not in _ORACLE_W:
+        W = OracleWeights(shape)
+        for l in range(layers):
+            Cc._weights(W, l, np.float32)
+            W.drop_layer(l)
+        for g in ("embed", "gf", "lm"):
+            Cc._global(W, g, np.float32)
+        W._embed = W._lm = None
+        _ORACLE_W[key] = W
+    W = _ORACLE_W[key]
+    wl = config_workload("C2")
+    pre, tok = [], 0
+    for r in wl.requests:
+        if tok + len(r.prompt) > 2048:
+            break
+        pre.append(r.prompt)
+        tok += len(r.prompt)
+    rng = np.random.default_rng(0)
+    hd, hkv = full.head_dim, full.n_kv_heads
+
+    kvkey = ("kv", layers, b)
+    if kvkey not in _ORACLE_W:   # seeded K/V of the decode requests, drawn once (setup, untimed)
+        _ORACLE_W[kvkey] = [[(rng.standard_normal((len(r.prompt), hkv, hd), dtype=np.float32),
+                              rng.standard_normal((len(r.prompt), hkv, hd), dtype=np.float32))
+                             for _ in range(layers)] for r in wl.requests[:b]]
+
+    def caches_for_decode():
+        cs = []
+        for r, kv in zip(wl.requests[:b], _ORACLE_W[kvkey]):
+            c = Cc.Cache(layers)
+            for l in range(layers):
+                c.k[l], c.v[l] = kv[l]     # a step appends by concatenation: the drawn arrays stay intact
+            c.T = len(r.prompt)
+            cs.append(c)
+        return cs
+
+    def run(lys):
+        cs = [Cc.Cache(layers) for _ in pre]
+        dec = caches_for_decode()
+        toks = [[int(t)] for t in rng.integers(0, full.vocab, size=b)]
+        t0 = time.perf_counter()
+        Cc.forward_rows(W, cs, pre, layers=lys, dtype=np.float32)
+        for _ in range(n_dec):
+            lg = Cc.forward_rows(W, dec, toks, layers=lys, dtype=np.float32)
+            toks = [[int(t)] for t in np.argmax(lg, -1)]
+        return time.perf_counter() - t0
+
+    with _blas_threads():
+        t_l = run(range(layers))
+        if ("t0", n_dec, b) not in _ORACLE_W:   # the 0-layer part (embedding + LM head), measured once
+            _ORACLE_W[("t0", n_dec, b)] = run([])
+        t_0 = _ORACLE_W[("t0", n_dec, b)]
+    per_layer = max(t_l - t_0, 0.0) / layers
+    scaled = t_0 + per_layer * full.n_layers
+    gen = len(pre) + n_dec * b
+    return {"value": gen / scaled, "unit": UNIT, "seconds": round(t_l + t_0, 2), "scaled_seconds": round(scaled, 2),
+            "generated": gen,
+            "sample": f"C2 slice: one {tok}-token prefill ({len(pre)} C2 prompts) + {n_dec} decode steps at b={b} "
+                      f"(contexts = C2 prompt lengths, seeded random K/V), {layers}/{full.n_layers} Llama-2-7B "
+                      f"layers + LM head, numpy fp32, per-request KV cache; per-layer time scaled to "
+                      f"{full.n_layers} layers"}
+
+
+def oracle_sched_c5():
+    """Reference-scheduler decisions/s on the C5 request set (4,096 requests,
+    8 stages, KV-capped to 24,000 blocks = C5-cap, synthetic frozen profile):
+    decision-log lines per second of oracle/scheduler.py."""
+    from oracle.scheduler import SchedOptions, schedule
+    from workload import synthetic_profile
+    wl = config_workload("C5")
+    reqs = [(len(r.prompt), r.predicted_len, r.max_new_tokens) for r in wl.requests]
+    tdec, tpre = synthetic_profile(1024, 2048, knee=64)
+    t0 = time.perf_counter()
+    s = schedule(reqs, SchedOptions(n_stages=8, block_size=16, kv_blocks=24000), tdec, tpre)
+    dt = time.perf_counter() - t0
+    return {"value": len(s.log) / dt, "unit": "decisions/s", "seconds": round(dt, 2), "decisions": len(s.log),
+            "micro_batches": len(s.plan),
+            "sample": "oracle/scheduler.py on C5 (4096 requests, W=8, kv_blocks=24000), decision-log lines/s"}
+
+
+def cpu_baseline(with_c1=True, with_sched=True):
+    c2 = oracle_c2_slice(layers=1)
+    out = {"value": c2["value"], "unit": UNIT, "kind": "oracle", "sample": c2["sample"], "c2_slice": c2}
+    out.update(host_info())
+    if with_c1:
+        out["c1_e2e"] = oracle_c1()
+    if with_sched:
+        out["sched_c5"] = oracle_sched_c5()
+    return out
+
+
 def run_reference(args):
+    """The tier's reference arm: the oracle as it stands on the host cores;
+    one step = the C2 slice (a bounded sample of the bench workload)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     vals, secs = [], []
     desc = ""
     for i in range(args.warmup + args.steps):
-        v, dt, desc = oracle_sample()
+        r = oracle_c2_slice(layers=1, n_dec=2)
+        desc = r["sample"]
         if i >= args.warmup:
-            vals.append(v)
-            secs.append(dt)
+            vals.append(r["value"])
+            secs.append(r["seconds"])
     value = statistics.mean(vals)
+    cb = {"value": value, "unit": UNIT, "kind": "oracle", "sample": desc}
+    cb.update(host_info())
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args), "cpu_baseline": cb,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -188,6 +323,55 @@ def _traffic_record(kernel):
         return None
     rec = json.load(open(files[-1]))
     rec["file"] = os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))
+    return rec
+
+
+# ----------------------------------------------------------- C5 stage record
+DEC_CLASSES = ["decode_attn", "gemm_qkv_dec", "gemm_o_dec", "gemm_gu_dec", "gemm_down_dec", "lm_head_dec"]
+PRE_CLASSES = ["prefill_attn", "gemm_qkv_pre", "gemm_o_pre", "gemm_gu_pre", "gemm_down_pre", "lm_head_pre"]
+
+
+def c5_stage(peaks, iters=10):
+    """The headline config's per-stage hot path (BASELINE configs[4]: Llama-2-70B,
+    8-stage pipeline => 10 of 80 layers per stage), measured on this GPU with
+    td_bench_step: decode micro-batches of b = 64 / 256 / 512 sequences at the
+    C5 workload's representative context (mean prompt + half the mean
+    predicted output) and a 2,048-token prefill (8 x 256).
+    Per kernel class: achieved bytes/s and FLOP/s and the fraction of its
+    attainable roofline max(bytes / HBM, FLOPs / TC) / time (GQA-8 decode
+    attention and the tensor-bound decode GEMMs at b = 512).  Parity of this
+    shape is tests/test_gpu_parity.py::test_llama70b_shaped_layer_gqa8*.
+    The stage here also holds the embedding and LM head (the last stage)."""
+    from paper_2506_10470_b200 import TD_BATCH_DECODE, TD_BATCH_PREFILL, TDPipe
+    shape = SHAPES["llama2_70b"].with_layers(10)
+    wl = config_workload("C5")
+    n_req = len(wl.requests)
+    L = np.array([len(r.prompt) for r in wl.requests])
+    P = np.array([r.predicted_len for r in wl.requests])
+    ctx_rep = int(L.sum() // n_req + (P.sum() // n_req) // 2)
+    t = TDPipe(shape, 1, device=0, kv_blocks=12288, hbm_peak_gbs=peaks["hbm"], tc_peak_tflops=peaks["tc_sus"])
+    rec = {"model": "Llama-2-70B-shaped, 10 of 80 layers (one stage of the 8-stage pipeline) + embedding + LM head",
+           "ctx_rep": ctx_rep, "peak_hbm_gbs": peaks["hbm"], "peak_tc_tflops": peaks["tc_sus"],
+           "parity": "tests/test_gpu_parity.py::test_llama70b_shaped_layer_gqa8 (+ _large_decode_batch)", "steps": {}}
+    for label, kind, n, ln, classes in [("decode_b64", TD_BATCH_DECODE, 64, ctx_rep, DEC_CLASSES),
+                                        ("decode_b256", TD_BATCH_DECODE, 256, ctx_rep, DEC_CLASSES),
+                                        ("decode_b512", TD_BATCH_DECODE, 512, ctx_rep, DEC_CLASSES),
+                                        ("prefill_T2048", TD_BATCH_PREFILL, 8, 256, PRE_CLASSES)]:
+        us, ideal = t.td_bench_step(kind, n, ln, iters)
+        ks = {}
+        for name in classes:
+            v = t.td_get_timing(name)
+            if v["ms"] <= 0:
+                continue
+            sec = v["ms"] * 1e-3
+            att = max(v["bytes"] / (peaks["hbm"] * 1e9), v["flops"] / (peaks["tc_sus"] * 1e12))
+            ks[name] = {"launches": v["launches"], "us_per_launch": round(v["ms"] * 1e3 / v["launches"], 2),
+                        "GB/s": round(v["bytes"] / sec / 1e9, 1), "TFLOP/s": round(v["flops"] / sec / 1e12, 1),
+                        "bound": "tensor" if v["flops"] / (peaks["tc_sus"] * 1e12) > v["bytes"] / (peaks["hbm"] * 1e9)
+                        else "hbm", "frac": round(att / sec, 4)}
+        rec["steps"][label] = {"n_seqs": n, "len": ln, "us": round(us, 1), "ideal_us": round(ideal, 1),
+                               "sol_frac": round(ideal / us, 4) if us else None, "kernels": ks}
+    t.close()
     return rec
 
 
@@ -321,11 +505,11 @@ def run_ours(args):
                                         traffic_ratio=round(tf["ratio"], 4), traffic_src=tf["file"])
         line["kernels"] = rl
         line["kernel_share"] = share
-    if not args.no_cpu_baseline:
-        v, dt, desc = oracle_sample()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc,
-                                "seconds": round(dt, 2)}
     t.close()
+    if not args.no_c5_stage:
+        line["c5_stage"] = c5_stage(peaks)
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
     return 0
 
@@ -489,6 +673,7 @@ def main():
     ap.add_argument("--sigma", type=int, default=1)
     ap.add_argument("--no-timing", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5-stage", action="store_true")
     ap.add_argument("--handoff", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--kv-blocks", type=int, default=0)
     args = ap.parse_args()

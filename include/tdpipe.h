@@ -72,8 +72,10 @@ typedef int32_t td_status;
 /* Host all-gather across the ranks of a multi-process pipeline: every rank
  * passes `bytes` bytes in `send`; on return `recv` holds world_size * bytes,
  * rank r's contribution at offset r * bytes.  Returns 0 on success.  Provided
- * by the caller (e.g. torch.distributed over gloo); called only from td_create
- * and td_profile, on the calling thread, in the same order on every rank. */
+ * by the caller (e.g. torch.distributed over gloo); called only from td_create,
+ * td_profile, td_run (when the request set needs larger hand-off slots than
+ * the mailboxes hold -- every rank decides identically) and td_destroy, on the
+ * calling thread, in the same order on every rank. */
 typedef int32_t (*td_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
 
 /* Model shape (Llama-style pre-norm decoder; Table 2). */
@@ -252,10 +254,12 @@ td_status td_get_log(struct td_ctx* ctx, char* buf, size_t cap, size_t* need);
  * per-stage B200 times.  Needs a loaded profile table. */
 td_status td_simulate(struct td_ctx* ctx, td_run_stats* st, int64_t host_return_ns);
 
-/* Write the last td_simulate run as a Chrome trace (chrome://tracing /
+/* Write the last td_simulate run -- or the last td_run executed with timing
+ * on (td_set_timing(ctx, 1): spans are CUDA events on the library stream, ns
+ * from the run's first launch) -- as a Chrome trace (chrome://tracing /
  * Perfetto JSON): one complete event per (micro-batch, stage) on thread =
- * stage, plus a "kv_used_blocks" counter track sampled at every launch
- * (the KV-usage timeline of PAPER.md:580-585 fig:memory_usage). */
+ * stage, plus a "kv_used_blocks" counter track sampled at every launch (the
+ * KV-usage timeline of PAPER.md:580-585 fig:memory_usage). */
 td_status td_write_trace(struct td_ctx* ctx, const char* path);
 
 /* Model / pool facts: kv_blocks, layers of `stage`, weight bytes per stage. */
@@ -269,21 +273,37 @@ td_status td_set_timing(struct td_ctx* ctx, int32_t on);
 td_status td_get_timing(struct td_ctx* ctx, const char* name, int64_t* launches,
                         double* total_ms, double* bytes, double* flops);
 
+/* Stage step benchmark (testing / measurement): one synthetic micro-batch
+ * through every stage this process holds, `iters` times after 2 warm-up
+ * passes -- kind DECODE: n_seqs sequences at context `len` (each decodes the
+ * token at position len-1, pages scattered over the pool); kind PREFILL:
+ * n_seqs prompts of `len` tokens.  *step_us = mean device microseconds of one
+ * pass (CUDA events on the library stream), *ideal_us (nullable) = its speed
+ * of light max(bytes / hbm_peak_gbs, FLOPs / tc_peak_tflops) with the
+ * td_run_stats accounting (0 if the peaks are unset).  Per-kernel timing of
+ * the timed passes is left in the td_get_timing accumulators.  Clears the KV
+ * pool.  TD_ERANGE if n_seqs * ceil(len/16) > kv_blocks. */
+td_status td_bench_step(struct td_ctx* ctx, int32_t kind, int32_t n_seqs, int32_t len, int32_t iters,
+                        double* step_us, double* ideal_us);
+
 /* Kernel unit test (testing only): out[T, N] fp32 = A[T, K] . W[N, K]^T with
- * A, W given as bf16 bit patterns (host).  impl 0 = tcgen05 kernel,
- * 1 = mma.sync baseline; splits > 1 exercises the split-K reduction.  Runs on
- * `device`, allocates and frees its own buffers, synchronous.  impl 0 packs W
- * into the tile-packed layout the engine uses; impl 2 = tcgen05 with row-major
- * W through a TMA descriptor; impl 3 = the stream-K decode kernel (T <= 128,
- * packed W). */
+ * A, W given as bf16 bit patterns (host), on the tcgen05 kernels: impl 0
+ * packs W into the tile-packed layout the engine uses, impl 2 reads row-major
+ * W through a TMA descriptor; splits > 1 exercises the split-K reduction
+ * (T > 128 with impl 0 and splits == 1: the persistent token-major prefill
+ * kernel); impl 4 = the token-major kernel with `splits` K splits (T > 128;
+ * the engine's path for 129+-token decode micro-batches).  Runs on `device`,
+ * allocates and frees its own buffers, synchronous.  TD_EINVAL for any other
+ * impl. */
 td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N, int32_t K,
                        int32_t impl, int32_t splits, float* out);
 
 /* GEMM timing sweep (testing only): average device microseconds per call of
  * the tcgen05 GEMM on [T, K] x [N, K]^T (tile-packed weights, fp32 output),
  * cycling over `copies` weight buffers so that the weights stream from HBM;
- * splits = split-K count (1 = none); decode = 1 selects decode token tiles,
- * decode = 2 the stream-K decode kernel (T <= 128). */
+ * splits = split-K count (1 = none); decode = 1 selects the swap-AB decode
+ * kernel (weight rows x token tiles), decode = 2 the token-major kernel with
+ * `splits` K splits (reduction + epilogue launch included). */
 td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t splits, int32_t decode,
                         int32_t iters, int32_t copies, float* us_per_call);
 
@@ -291,9 +311,11 @@ td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t
  * per decode-attention launch for n sequences of context lengths ctx[n] (host),
  * H query / Hkv kv heads of size hd, pages scattered through a pool rotated
  * over enough copies (<= 400 MiB) that K/V stream from HBM, launched with
- * the engine's plan.  K/V, q are zeros (timing only). */
+ * the engine's plan (split = 0) or with `split`-token splits (a multiple of
+ * 16, >= 32); impl 0 = the engine's kernel choice, 1 = the SIMT kernel,
+ * 2 = the tensor-core kernel (hd 64 / 128).  K/V, q are zeros (timing only). */
 td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx, int32_t H, int32_t Hkv, int32_t hd,
-                        int32_t iters, float* us_per_call);
+                        int32_t iters, int32_t split, int32_t impl, float* us_per_call);
 
 /* Weight read-back (testing only): the bf16 bit patterns of F9 tensor
  * `tensor_id` (SURVEY.md §8(c) F9 enumeration: 0 = embedding [V, d]; layer l:

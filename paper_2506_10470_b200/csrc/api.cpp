@@ -241,6 +241,16 @@ extern "C" td_status td_run(td_ctx* c, td_run_stats* st) {
                         std::chrono::steady_clock::now() - t0).count();
   }
   c->log = ctl.log();
+  if (c->engine) {   // a timed run leaves its CUDA-event spans + KV timeline for td_write_trace
+    std::vector<TraceSpan> sp;
+    std::vector<std::pair<int64_t, int64_t>> kv;
+    c->engine->get_trace(&sp, &kv);
+    if (!sp.empty()) {
+      c->spans.clear();
+      for (const auto& x : sp) c->spans.push_back({x.mid, x.kind, x.stage, x.a_ns, x.b_ns});
+      c->kv_samples = kv;
+    }
+  }
   c->n_out.assign(c->reqs.size(), 0);
   int64_t gen = 0;
   for (size_t i = 0; i < c->reqs.size(); ++i) { c->n_out[i] = ctl.reqs()[i].n_out; gen += c->n_out[i]; }
@@ -527,6 +537,18 @@ extern "C" td_status td_info(td_ctx* c, int64_t* kv_blocks, int32_t* n_stages, i
   if (n_stages) *n_stages = c->n_stages;
   if (weight_bytes_stage0) *weight_bytes_stage0 = c->engine ? c->engine->weight_bytes_stage0() : 0;
   if (kv_bytes_per_block) *kv_bytes_per_block = c->engine ? c->engine->kv_bytes_per_block() : 0;
+  return TD_OK;
+}
+
+extern "C" td_status td_bench_step(td_ctx* c, int32_t kind, int32_t n_seqs, int32_t len, int32_t iters,
+                                   double* step_us, double* ideal_us) {
+  if (!c || !step_us || (kind != TD_BATCH_PREFILL && kind != TD_BATCH_DECODE)) return TD_EINVAL;
+  if (!c->engine) return fail(c, TD_ESTATE, "null executor");
+  double ms = 0, ideal = 0;
+  if (td_status st = c->engine->bench_step(kind == TD_BATCH_PREFILL, n_seqs, len, iters, &ms, &ideal))
+    return fail(c, st, c->engine->error);
+  *step_us = ms * 1e3;
+  if (ideal_us) *ideal_us = ideal * 1e3;
   return TD_OK;
 }
 

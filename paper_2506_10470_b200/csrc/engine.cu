@@ -29,6 +29,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "engine.h"
@@ -133,6 +134,11 @@ class CudaEngine : public Engine {
   }
   bool get_timing(const std::string& name, KernelTiming* t) override;
   td_status get_weight(int tid, std::vector<uint16_t>* out, int64_t* rows, int64_t* cols) override;
+  td_status bench_step(bool prefill, int n, int len, int iters, double* step_ms, double* ideal_ms) override;
+  void get_trace(std::vector<TraceSpan>* spans, std::vector<std::pair<int64_t, int64_t>>* kv) override {
+    *spans = trace_spans_;
+    *kv = trace_kv_;
+  }
 
  private:
   void release();
@@ -149,6 +155,8 @@ class CudaEngine : public Engine {
            bool defer = false);
   int tbegin(int cls);
   void tend(int idx, double bytes, double flops);
+  double accumulate_timed();
+  void fill_attn_work(size_t t0, int n, const int* q_start, const int* q_len, int T);
   int ring_acquire();
 
   td_model_shape s_{};
@@ -180,7 +188,8 @@ class CudaEngine : public Engine {
   int64_t rx_T_ = 0, tok_n_ = 0;         // rows per residual slot, pairs per token slot
   int64_t tok_off_ = 0, rx_off_ = 0;
   uint32_t fwd_out_ = 0, fwd_in_ = 0, tok_out_ = 0, tok_in_ = 0;   // monotone over the ctx lifetime
-  td_status peer_init();
+  td_status peer_init(int64_t rx_T, int64_t tok_n);
+  td_status peer_release();
   td_status allgather(const void* send, void* recv, size_t bytes);
   td_status flag_wait(cudaStream_t s, const char* base, int off, uint32_t v);
   td_status flag_write(cudaStream_t s, char* base, int off, uint32_t v);
@@ -199,6 +208,8 @@ class CudaEngine : public Engine {
   // kv
   bf16* kv_ = nullptr;
   int64_t C_ = 0, kv_block_bytes_layer_ = 0;
+  CUtensorMap kvmap_{};          // TMA view of the KV pool (tensor-core GQA decode attention)
+  bool have_kvmap_ = false;
   float* rope_ = nullptr;
   TcOperand tlm_;
   XOps xa_, xo_, xh_;
@@ -248,6 +259,14 @@ class CudaEngine : public Engine {
                                       "decode_attn@b129+", "gemm_dec@b1-8", "gemm_dec@b9-32", "gemm_dec@b33-128",
                                       "gemm_dec@b129+"};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev_;
+  // trace of a timed run: (micro-batch, kind, stage, timed_ index of its span),
+  // (timed_ index of the micro-batch's first span, KV blocks in use at launch)
+  int64_t cur_mid_ = 0;
+  char cur_kind_ = 'D';
+  std::vector<std::tuple<int64_t, char, int, int>> tr_;
+  std::vector<std::pair<int, int64_t>> tr_kv_;
+  std::vector<TraceSpan> trace_spans_;
+  std::vector<std::pair<int64_t, int64_t>> trace_kv_;
 };
 
 enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
@@ -422,8 +441,15 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   if (C_ < 1) { error = "no room for the KV pool"; return TD_ENOMEM; }
   if (cudaMalloc(&kv_, C_ * per_block) != cudaSuccess) { error = "KV pool allocation failed"; return TD_ENOMEM; }
   CK(cudaMemsetAsync(kv_, 0, C_ * per_block, st_));
+  if (hd_ >= 64 && H_ != Hkv_) {
+    have_kvmap_ = make_kv_map(&kvmap_, kv_, C_, Hkv_, hd_, own_l1_ - own_l0_);
+    if (!have_kvmap_) { error = "cuTensorMapEncodeTiled failed (KV pool)"; return TD_ECUDA; }
+  }
   if (peer_)
-    if (td_status e3 = peer_init()) return e3;
+    if (td_status e3 = peer_init(std::max<int64_t>({(int64_t)o.prefill_token_budget, (int64_t)s.max_seq_len,
+                                                    (int64_t)o.max_batch_seqs + std::max(o.hb_tokens, 0)}),
+                                 (int64_t)o.max_batch_seqs + std::max(o.hb_tokens, 0)))
+      return e3;
   CK(cudaEventCreate(&ev_start_));
   CK(cudaEventCreate(&ev_end_));
   for (int i = 0; i < kRing; ++i) CK(cudaEventCreateWithFlags(&ring_ev_[i], cudaEventDisableTiming));
@@ -434,16 +460,7 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
 void CudaEngine::release() {
   if (st_) cudaStreamSynchronize(st_);
   if (tst_) cudaStreamSynchronize(tst_);
-  if (peer_ && mbox_) {
-    // every rank is done storing into its neighbours' mailboxes before any is freed
-    int one = 1;
-    std::vector<int> all(world_);
-    allgather(&one, all.data(), sizeof one);
-    for (auto& kv : peer_mbox_) cudaIpcCloseMemHandle(kv.second);
-    peer_mbox_.clear();
-    cudaFree(mbox_);
-    mbox_ = nullptr;
-  }
+  if (peer_ && mbox_) peer_release();   // every rank is done storing into its neighbours' mailboxes first
   cudaFree(wbuf_);
   cudaFree(kv_);
   cudaFree(rope_);
@@ -502,8 +519,8 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
                                 std::min<int64_t>(n, kAttnSmallN) * cdiv(s_.max_seq_len, kAttnMinSplitGQA));
   CK(cudaMalloc(&part_, part_cap_ * H_ * (hd_ + 2) * 4));
   cudaFree(attn_cnt_);
-  CK(cudaMalloc(&attn_cnt_, n * Hkv_ * sizeof(int)));
-  CK(cudaMemsetAsync(attn_cnt_, 0, n * Hkv_ * sizeof(int), st_));
+  CK(cudaMalloc(&attn_cnt_, (n * Hkv_ + 2) * sizeof(int)));   // + the tensor-core kernel's work counters
+  CK(cudaMemsetAsync(attn_cnt_, 0, (n * Hkv_ + 2) * sizeof(int), st_));
   // metadata ring: per seq 5 ints + bt, per token 4 ints, header
   const int64_t need = 16 + 5 * n + 2 + n * maxblk + 4 * T + 64;
   if (need > meta_cap_) {
@@ -557,29 +574,34 @@ td_status CudaEngine::make_x_ops() {
 // consumes the partials (launch_resid_norm).
 int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
                      bool defer) {
-  if (gemm_sk_applies(W, T, decode)) {   // stream-K weight streaming, epilogue applied in-kernel
-    launches_ += 1;
-    return launch_gemm_sk(W, xo.by_bn, T, ep, ws_, counters_ + kSkTicketOff, st_);
-  }
   int splits = 1;
-  // 129..256-token decode batches of the wide GEMMs (QKV, gate/up, LM head) are
-  // closer to the tensor roof than to HBM: take the token-major kernel
-  static const bool dec_tn = !getenv("TDPIPE_DEC_TN") || atoi(getenv("TDPIPE_DEC_TN"));   // A/B knob
-  if (decode && T > 128 && N >= 8192 && dec_tn) decode = false;
-  if (decode) {
+  if (decode && T > 128) {
+    // 129..512-token decode batches are near (or past) the tensor roof: the
+    // token-major kernel (128 tokens x 256 features per tile), with split-K
+    // when the tiles alone fill the 148 SMs badly: the split count (<= 8,
+    // >= 8 k-blocks per split, partials within the L2-sized workspace) that
+    // maximises the persistent grid's occupancy units / (rounds x 148); ties
+    // keep fewer splits
+    decode = false;
+    const int64_t tiles = (int64_t)((T + 127) / 128) * ((N + 255) / 256);
+    double best = 0.0;
+    for (int sp = 1; sp <= 8; ++sp) {
+      if (sp > 1 && ((K / 64) / sp < 8 || (int64_t)sp * T * ((N + 127) / 128 * 128) > ws_cap_)) break;
+      const int64_t units = tiles * sp;
+      const double eff = (double)units / (double)(((units + 147) / 148) * 148);
+      if (eff > best + 0.02) {
+        best = eff;
+        splits = sp;
+      }
+    }
+  } else if (decode) {
+    // split-K to ~288 CTAs (about 2 per SM), at most 8 splits, >= 4 k-blocks
+    // per split, partials within the workspace (scripts/gemm_sweep.py)
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
-    static const int64_t target = getenv("TDPIPE_SPLIT_TARGET") ? atoi(getenv("TDPIPE_SPLIT_TARGET")) : 288;
-    static const int64_t smax = getenv("TDPIPE_SPLIT_MAX") ? atoi(getenv("TDPIPE_SPLIT_MAX")) : 8;   // A/B knob
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(smax, target / ctas));
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, 288 / ctas));
     while (splits > 1 && (K / 64) / splits < 4) --splits;
     while (splits > 1 && (int64_t)splits * T * ((N + 127) / 128 * 128) > ws_cap_) --splits;
-    // A/B knobs: cap the split count of the QKV GEMM (its reduce is a separate
-    // RoPE / KV-scatter kernel) or of the residual GEMMs (reduced in resid_norm)
-    static const int cap_qkv = getenv("TDPIPE_SPLITS_QKV") ? atoi(getenv("TDPIPE_SPLITS_QKV")) : 8;
-    static const int cap_res = getenv("TDPIPE_SPLITS_RESID") ? atoi(getenv("TDPIPE_SPLITS_RESID")) : 8;
-    if (ep.mode == kEpiQKV) splits = std::max(1, std::min(splits, cap_qkv));
-    if (ep.mode == kEpiResid) splits = std::max(1, std::min(splits, cap_res));
   }
   const int used = launch_gemm_tc(W, xo.by_bn, T, ep, splits, ws_, counters_, decode, st_, defer);
   launches_ += (used > 1 && !defer) ? 2 : 1;
@@ -649,6 +671,28 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
 }
 
 // ------------------------------------------------------------------ timing
+// fold the recorded (event pair, class) spans into timing_acc_; returns the
+// summed stage-busy milliseconds.  The stream must be synchronised.
+double CudaEngine::accumulate_timed() {
+  double busy = 0;
+  for (auto& tl : timed_) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, tl.a, tl.b);
+    for (int c : {tl.cls, tl.sub}) {
+      if (c < 0) continue;
+      KernelTiming& kt = timing_acc_[cls_names_[c]];
+      kt.launches++;
+      kt.ms += t;
+      kt.bytes += tl.bytes;
+      kt.flops += tl.flops;
+    }
+    if (tl.cls == cStage) busy += t;
+  }
+  timed_.clear();
+  ev_used_ = 0;
+  return busy;
+}
+
 int CudaEngine::tbegin(int cls) {
   if (!timing_) return -1;
   if (ev_used_ + 2 > ev_pool_.size()) {
@@ -675,6 +719,24 @@ void CudaEngine::tend(int idx, double bytes, double flops) {
   cudaEventRecord(tl.b, st_);
 }
 
+// algorithmic work of the attention launches recorded since timed_[t0]:
+// decode attention reads every context token's K and V (2*Hkv*hd*2 bytes per
+// layer) + q and o; prefill attention does the causal QK^T
+// and PV, 4*H*hd FLOPs per (query, key <= query) pair
+void CudaEngine::fill_attn_work(size_t t0, int n, const int* q_start, const int* q_len, int T) {
+  double kvb = 0;
+  for (int i = 0; i < n; ++i) kvb += (double)(q_start[i] + q_len[i]);
+  kvb = kvb * 2.0 * Hkv_ * hd_ * 2 + 4.0 * n * H_ * hd_;
+  double pf = 0;
+  for (int i = 0; i < n; ++i) pf += 0.5 * (double)q_len[i] * (q_len[i] + 1);
+  pf *= 4.0 * H_ * hd_;
+  const double pb = (double)T * (2.0 * H_ * hd_ * 2 + 2.0 * Hkv_ * hd_ * 2);
+  for (size_t k = t0; k < timed_.size(); ++k) {
+    if (timed_[k].cls == cDecAttn) timed_[k].bytes = kvb;
+    if (timed_[k].cls == cPreAttn) { timed_[k].flops = pf; timed_[k].bytes = pb; }
+  }
+}
+
 bool CudaEngine::get_timing(const std::string& name, KernelTiming* t) {
   auto it = timing_acc_.find(name);
   if (it == timing_acc_.end()) { *t = KernelTiming(); return true; }
@@ -686,20 +748,10 @@ bool CudaEngine::get_timing(const std::string& name, KernelTiming* t) {
 td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int32_t* arena, float* xpeer,
                                 bool* sent) {
   if (sent) *sent = false;
-  // A/B knobs (decode micro-batches of >= X tokens launch without PDL):
-  // whole micro-batch / attention + its successor / GEMMs
-  static const int nopdl_t = getenv("TDPIPE_NOPDL_T") ? atoi(getenv("TDPIPE_NOPDL_T")) : 1 << 30;
-  static const int nopdl_attn = getenv("TDPIPE_NOPDL_ATTN_T") ? atoi(getenv("TDPIPE_NOPDL_ATTN_T")) : 1;
-  static const int nopdl_gemm = getenv("TDPIPE_NOPDL_GEMM_T") ? atoi(getenv("TDPIPE_NOPDL_GEMM_T")) : 1 << 30;
-  const bool big = !M.prefill && M.T >= nopdl_t;
-  static const int nopdl_o = getenv("TDPIPE_NOPDL_O_T") ? atoi(getenv("TDPIPE_NOPDL_O_T")) : 1 << 30;
-  const bool big_attn = !M.prefill && M.T >= nopdl_attn;
-  const bool big_o = !M.prefill && M.T >= nopdl_o;
-  const bool big_gemm = !M.prefill && M.T >= nopdl_gemm;
-  pdl_suppress(big);
-  struct Restore {
-    ~Restore() { pdl_suppress(false); }
-  } restore_pdl;
+  // Decode attention is launched without PDL (a PDL dependent, it made decode
+  // steps 2-10 % slower at b >= 8: profiles/r1/pdl_ab.md); every other hot
+  // kernel is a PDL dependent of its predecessor.
+  const bool attn_nopdl = !M.prefill;
   const int T = M.T, n = M.n;
   const int nqkv = (H_ + 2 * Hkv_) * hd_;
   const float eps = s_.rms_eps;
@@ -730,13 +782,13 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ep.hd = hd_;
     const int iq = tbegin(cQKV + (M.prefill ? 0 : kDecOff));
     if (iq >= 0 && !M.prefill) timed_[iq].sub = kGemmBucket + bucket_of(T);
-    if (big_gemm) pdl_suppress(true);
     // pure decode: the QKV split-K reduction (+ RoPE + K/V write) is left to
     // the attention kernel (DecodeAttnParams::qkv_ws) -- one launch fewer
-    static const bool fuse_qkv = !getenv("TDPIPE_FUSE_QKV") || atoi(getenv("TDPIPE_FUSE_QKV"));
-    const bool defer_qkv = dec && !M.hybrid && fuse_qkv;
+    // (not for the tensor-core GQA kernel: its single q-prep warp would redo
+    // the reduction for every split item of a sequence; the split-K reduce
+    // kernel does it once per token and the kernel bulk-copies q)
+    const bool defer_qkv = dec && !M.hybrid && !(have_kvmap_ && Hkv_ < H_);
     const int qsplits = gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec, /*defer=*/defer_qkv);
-    pdl_suppress(big);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.hybrid) {
       // PP+HB: decode members [0, nd) -- one token each, so token row = member
@@ -746,10 +798,13 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
         DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, M.nd, H_, Hkv_, hd_, 0,
                             attn_cnt_};
         dp.part_cap = part_cap_;
+        dp.kvmap = have_kvmap_ ? &kvmap_ : nullptr;
+        dp.layer = l - own_l0_;
+        dp.work = attn_cnt_ + capN_ * Hkv_;
         plan_decode_attn(dp, mb_ctx_.data());
-        if (M.nd >= nopdl_attn) pdl_suppress(true);
+        pdl_suppress(true);
         launch_decode_attn(dp, st_);
-        pdl_suppress(big);
+        pdl_suppress(false);
         launches_++;
       }
       if (M.nd < n) {
@@ -772,6 +827,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, n, H_, Hkv_, hd_, 0,
                           attn_cnt_};
       dp.part_cap = part_cap_;
+      dp.kvmap = have_kvmap_ ? &kvmap_ : nullptr;
+      dp.layer = l - own_l0_;
+      dp.work = attn_cnt_ + capN_ * Hkv_;
       if (defer_qkv && qsplits > 1) {
         dp.qkv_ws = ws_;
         dp.qkv_splits = qsplits;
@@ -781,9 +839,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       plan_decode_attn(dp, mb_ctx_.data());
       const int ida = tbegin(cDecAttn);
       if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
-      if (big_attn) pdl_suppress(true);
+      pdl_suppress(attn_nopdl);
       launch_decode_attn(dp, st_);
-      pdl_suppress(big);
+      pdl_suppress(false);
       tend(ida, 0, 0);   // bytes filled by the caller-side accumulator (ctx-dependent)
       launches_++;
     }
@@ -793,9 +851,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eo.ldo = d_;
     const int io = tbegin(cO + (M.prefill ? 0 : kDecOff));
     if (io >= 0 && !M.prefill) timed_[io].sub = kGemmBucket + bucket_of(T);
-    if (big_o || big_gemm) pdl_suppress(true);
     const int so = gemm(xo_, w.to, T, d_, H_ * hd_, eo, dec, /*defer=*/true);
-    pdl_suppress(big);
     tend(io, (double)d_ * H_ * hd_ * 2 + (double)T * H_ * hd_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * H_ * hd_);
     if (so > 1) launch_resid_norm(ws_, so, x_, w.g2, a_, T, d_, eps, st_);   // reduce + residual + norm
     else launch_rmsnorm(x_, w.g2, a_, nullptr, T, d_, eps, st_);
@@ -805,9 +861,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     eg.out_bf16 = h_;
     const int ig = tbegin(cGU + (M.prefill ? 0 : kDecOff));
     if (ig >= 0 && !M.prefill) timed_[ig].sub = kGemmBucket + bucket_of(T);
-    if (big_gemm) pdl_suppress(true);
     gemm(xa_, w.tgu, T, 2 * F_, d_, eg, dec);
-    pdl_suppress(big);
     tend(ig, 2.0 * F_ * d_ * 2 + (double)T * d_ * 2 + (double)T * F_ * 2, 2.0 * T * 2 * F_ * d_);
     EpiParams ed{};
     ed.mode = kEpiResid;
@@ -815,9 +869,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     ed.ldo = d_;
     const int idn = tbegin(cDown + (M.prefill ? 0 : kDecOff));
     if (idn >= 0 && !M.prefill) timed_[idn].sub = kGemmBucket + bucket_of(T);
-    if (big_gemm) pdl_suppress(true);
     const int sd = gemm(xh_, w.td, T, d_, F_, ed, dec, /*defer=*/true);
-    pdl_suppress(big);
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
       const bool last_layer = l + 1 == stage_l1_[stage];
@@ -871,6 +923,7 @@ td_status CudaEngine::run_microbatch(const Meta& M, const int32_t* dm, int32_t* 
       xpeer = reinterpret_cast<float*>(rx_slot(peer_mbox_.at(rank_ + 1), seq));
     }
     const int is = tbegin(cStage);
+    if (is >= 0) tr_.emplace_back(cur_mid_, cur_kind_, s, is);
     bool sent = false;
     if (td_status e = run_stage(s, M, dm, arena, xpeer, &sent)) return e;
     tend(is, 0, 0);
@@ -997,6 +1050,19 @@ td_status CudaEngine::begin_run(const std::vector<HostReq>& reqs, bool record_lo
   for (auto& r : reqs) maxL = std::max<int64_t>(maxL, (int64_t)r.prompt.size() + r.max_new);
   const int64_t T = std::max<int64_t>(o_.prefill_token_budget, maxL);
   if (td_status e = ensure_work(T, std::max<int64_t>((int64_t)reqs.size(), 1), cdiv(maxL + 1, 16))) return e;
+  if (peer_) {
+    // hand-off slot sizes vs the largest micro-batch this request set can
+    // form: a decode micro-batch holds at most every live request, and a live
+    // request holds >= 1 KV block, so <= min(requests, C) sequences (+ the
+    // PP+HB prefill chunks); a prefill one <= max(budget, longest prompt incl.
+    // recompute).  Every rank sees the same requests, so all re-size together.
+    const int64_t nseq = std::min<int64_t>((int64_t)reqs.size(), C_) + std::max(o_.hb_tokens, 0);
+    const int64_t rxT = std::max<int64_t>({(int64_t)o_.prefill_token_budget, maxL, nseq});
+    if (rxT > rx_T_ || nseq > tok_n_) {
+      if (td_status e = peer_release()) return e;
+      if (td_status e = peer_init(std::max(rxT, rx_T_), std::max(nseq, tok_n_))) return e;
+    }
+  }
   record_ = record_logits;
   rec_.assign(record_logits ? reqs.size() : 0, {});
   launches_ = 0;
@@ -1067,6 +1133,13 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
   }
   Meta M = build_meta(r, mb.kind == 'P', n, mb.q_start.data(), mb.q_len.data(), aoff.data(), emit.data(), blocks,
                       nullptr, 0);
+  cur_mid_ = mb.mid;
+  cur_kind_ = mb.kind;
+  if (timing_) {   // KV-usage timeline (PAPER.md:580-585 fig:memory_usage): blocks held at this launch
+    int64_t used = 0;
+    for (const auto& rq : reqs) used += (int64_t)rq.blocks.size();
+    tr_kv_.emplace_back((int)timed_.size(), used);
+  }
   if (mb.kind == 'H') {
     M.hybrid = 1;
     M.nd = nd;
@@ -1081,24 +1154,10 @@ int CudaEngine::launch(const MicroBatch& mb, const std::vector<Req>& reqs) {
   h2d_bytes_ += (int64_t)M.total * 4;
   const size_t t0 = timed_.size();
   if (td_status e = run_microbatch(M, dmeta_[r], arena_)) return e;
-  if (timing_) {
-    // algorithmic bytes of decode attention: every context token's K and V
-    // (2*Hkv*hd*2 bytes per layer) + q and o
-    double kvb = 0;
-    for (int i = 0; i < n; ++i) kvb += (double)(mb.q_start[i] + mb.q_len[i]);
-    kvb = kvb * 2.0 * Hkv_ * hd_ * 2 + 4.0 * n * H_ * hd_;
-    // prefill attention FLOPs: causal QK^T and PV over each prompt, 4*H*hd per (q, k<=q) pair
-    double pf = 0;
-    for (int i = 0; i < n; ++i) pf += 0.5 * (double)mb.q_len[i] * (mb.q_len[i] + 1);
-    pf *= 4.0 * H_ * hd_;
-    const double pb = (double)M.T * (2.0 * H_ * hd_ * 2 + 2.0 * Hkv_ * hd_ * 2);
-    for (size_t k = t0; k < timed_.size(); ++k) {
-      if (timed_[k].cls == cDecAttn) timed_[k].bytes = kvb;
-      if (timed_[k].cls == cPreAttn) { timed_[k].flops = pf; timed_[k].bytes = pb; }
-    }
-  }
+  if (timing_) fill_attn_work(t0, n, mb.q_start.data(), mb.q_len.data(), M.T);
   cudaEventRecord(ring_ev_[r], st_);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = take_launch_error();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { error = std::string("launch: ") + cudaGetErrorString(e); return TD_ECUDA; }
   if (record_) {
     if (hlogits_cap_ < (int64_t)n * V_) {
@@ -1130,20 +1189,24 @@ td_status CudaEngine::end_run(td_run_stats* st) {
   float ms = 0.f;
   if (started_) CK(cudaEventElapsedTime(&ms, ev_start_, ev_end_));
   st->makespan_ns = (int64_t)((double)ms * 1e6);
-  double busy = 0;
-  for (auto& tl : timed_) {
-    float t = 0.f;
-    cudaEventElapsedTime(&t, tl.a, tl.b);
-    for (int c : {tl.cls, tl.sub}) {
-      if (c < 0) continue;
-      KernelTiming& kt = timing_acc_[cls_names_[c]];
-      kt.launches++;
-      kt.ms += t;
-      kt.bytes += tl.bytes;
-      kt.flops += tl.flops;
+  if (timing_ && started_) {   // the run's trace, in ns from its first launch
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev_start_, e);
+      return (int64_t)((double)t * 1e6);
+    };
+    trace_spans_.clear();
+    trace_kv_.clear();
+    for (const auto& x : tr_) {
+      const TimedLaunch& tl = timed_[std::get<3>(x)];
+      trace_spans_.push_back({std::get<0>(x), std::get<1>(x), std::get<2>(x), at(tl.a), at(tl.b)});
     }
-    if (tl.cls == cStage) busy += t;
+    for (const auto& kv : tr_kv_)
+      if (kv.first < (int)timed_.size()) trace_kv_.emplace_back(at(timed_[kv.first].a), kv.second);
   }
+  tr_.clear();
+  tr_kv_.clear();
+  const double busy = accumulate_timed();
   if (timing_ && ms > 0) {
     st->bubble_frac = 1.0 - busy / ((double)S_ * ms);
     st->busy_ns[0] = (int64_t)(busy * 1e6 / S_);
@@ -1287,6 +1350,10 @@ td_status CudaEngine::stage_forward(int stage, const td_batch& b, const void* in
   }
   td_status e = run_stage(stage, M, dmeta_[r], tok);
   if (e == TD_OK) {
+    const cudaError_t le = take_launch_error();
+    if (le != cudaSuccess) { error = std::string("launch: ") + cudaGetErrorString(le); e = TD_ECUDA; }
+  }
+  if (e == TD_OK) {
     if (stage == S_ - 1) CK(cudaMemcpyAsync(out, logits_, (size_t)n * V_ * 4, cudaMemcpyDeviceToHost, st_));
     else CK(cudaMemcpyAsync(out, x_, (size_t)T * d_ * 4, cudaMemcpyDeviceToHost, st_));
   }
@@ -1409,6 +1476,78 @@ td_status CudaEngine::profile(int b_max, int k_max, int ctx_len, std::vector<int
   return TD_OK;
 }
 
+// -------------------------------------------------------------- bench step
+// One synthetic micro-batch through this process's stages, `iters` times:
+// decode = n sequences at context `len` (each decodes its token at position
+// len-1), prefill = n prompts of `len` tokens.  Pages are distinct and
+// scattered like the profile's.  Per-kernel CUDA-event timing accumulates into
+// timing_acc_ (cleared first); *step_ms = mean device time of one pass over
+// the stages, *ideal_ms = its speed of light max(bytes / HBM, FLOPs / TC)
+// under the td_options peaks (the td_run_stats accounting).
+td_status CudaEngine::bench_step(bool prefill, int n, int len, int iters, double* step_ms, double* ideal_ms) {
+  CK(cudaSetDevice(dev_));
+  if (n < 1 || len < 1 || iters < 1 || len > s_.max_seq_len) { error = "bad bench_step shape"; return TD_EINVAL; }
+  const int nb = (int)cdiv(len, 16);
+  if ((int64_t)n * nb > C_) { error = "KV pool too small for the bench step"; return TD_ERANGE; }
+  const int T = prefill ? n * len : n;
+  if (td_status e = ensure_work(T, n, nb)) return e;
+  int32_t* tok = nullptr;
+  CK(cudaMalloc(&tok, (size_t)T * 4));
+  CK(cudaMemsetAsync(tok, 0, (size_t)T * 4, st_));
+  std::vector<int32_t> bt((size_t)n * nb);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < nb; ++k) bt[(size_t)i * nb + k] = (int32_t)(((int64_t)k * n + i) % C_);   // interleaved pages
+  std::vector<int> qs(n, prefill ? 0 : len - 1), ql(n, prefill ? len : 1);
+  for (int i = 0; i < kRing; ++i) ring_used_[i] = false;
+  Meta M = build_meta(0, prefill, n, qs.data(), ql.data(), nullptr, nullptr, {}, bt.data(), nb);
+  CK(cudaMemcpyAsync(dmeta_[0], hmeta_[0], (size_t)M.total * 4, cudaMemcpyHostToDevice, st_));
+  const bool saved = timing_;
+  timing_ = false;
+  for (int w = 0; w < 2; ++w)
+    for (int s = own_s0_; s < own_s1_; ++s)
+      if (td_status e = run_stage(s, M, dmeta_[0], tok)) { cudaFree(tok); return e; }
+  timing_acc_.clear();
+  timed_.clear();
+  ev_used_ = 0;
+  timing_ = true;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st_));
+  for (int it = 0; it < iters; ++it) {
+    const size_t t0 = timed_.size();
+    for (int s = own_s0_; s < own_s1_; ++s)
+      if (td_status e = run_stage(s, M, dmeta_[0], tok)) { cudaFree(tok); timing_ = saved; return e; }
+    fill_attn_work(t0, n, qs.data(), ql.data(), T);
+  }
+  CK(cudaEventRecord(e1, st_));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  accumulate_timed();
+  timing_ = saved;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(tok);
+  *step_ms = ms / iters;
+  {   // speed of light of one pass (as launch())
+    const int nl = own_l1_ - own_l0_;
+    const double nqkv = (double)(H_ + 2 * Hkv_) * hd_;
+    const double w_layer = 2.0 * (nqkv * d_ + (double)d_ * H_ * hd_ + 2.0 * F_ * d_ + (double)d_ * F_ + 2.0 * d_);
+    const bool head = own_s1_ == S_;
+    const double kv_tok = 2.0 * Hkv_ * hd_ * 2;
+    const double ctx_sum = (double)n * len, att = prefill ? n * (0.5 * len * (len + 1.0)) : (double)n * len;
+    const double bytes = nl * (w_layer + ctx_sum * kv_tok + T * kv_tok) + (head ? 2.0 * V_ * d_ + 2.0 * d_ : 0.0);
+    const double flops = nl * (T * w_layer + 4.0 * H_ * hd_ * att) + (head ? 2.0 * n * V_ * d_ : 0.0);
+    *ideal_ms = (o_.hbm_peak_gbs > 0 && o_.tc_peak_tflops > 0)
+                    ? std::max(bytes / o_.hbm_peak_gbs, flops / (o_.tc_peak_tflops * 1e3)) / 1e6
+                    : 0.0;
+  }
+  CK(cudaMemsetAsync(kv_, 0, C_ * kv_block_bytes_layer_ * (own_l1_ - own_l0_), st_));
+  CK(cudaStreamSynchronize(st_));
+  return TD_OK;
+}
+
 // ------------------------------------------------------ peer-store hand-off
 td_status CudaEngine::allgather(const void* send, void* recv, size_t bytes) {
   if (!o_.allgather || o_.allgather(o_.allgather_user, send, recv, bytes) != 0) {
@@ -1439,10 +1578,10 @@ td_status CudaEngine::flag_write(cudaStream_t s, char* base, int off, uint32_t v
 // + its flag), s-1 (slot-free acks), and for stages 0 / S-1 each other (token
 // ring, token acks).  Slot capacities are fixed here from the options, so no
 // mailbox is ever reallocated (a micro-batch over them fails with TD_ERANGE).
-td_status CudaEngine::peer_init() {
-  rx_T_ = std::max<int64_t>({(int64_t)o_.prefill_token_budget, (int64_t)s_.max_seq_len,
-                             (int64_t)o_.max_batch_seqs + std::max(o_.hb_tokens, 0)});
-  tok_n_ = (int64_t)o_.max_batch_seqs + std::max(o_.hb_tokens, 0);
+td_status CudaEngine::peer_init(int64_t rx_T, int64_t tok_n) {
+  rx_T_ = rx_T;
+  tok_n_ = tok_n;
+  fwd_out_ = fwd_in_ = tok_out_ = tok_in_ = 0;   // a fresh mailbox: every flag is 0
   tok_off_ = 4096;
   rx_off_ = tok_off_ + cdiv((int64_t)kTokRing * 2 * tok_n_ * 4, 4096) * 4096;
   const int64_t bytes = rank_ == 0 ? rx_off_ : rx_off_ + (int64_t)kRx * rx_T_ * d_ * 4;
@@ -1467,6 +1606,22 @@ td_status CudaEngine::peer_init() {
   int one = 1;   // every mailbox is open (and its flags zeroed) before anyone stores into it
   std::vector<int> ok(world_);
   return allgather(&one, ok.data(), sizeof one);
+}
+
+// Every rank frees its mailbox after all ranks are done storing into it
+// (td_destroy, or a re-size in begin_run).
+td_status CudaEngine::peer_release() {
+  if (!mbox_) return TD_OK;
+  CK(cudaStreamSynchronize(st_));
+  if (tst_) CK(cudaStreamSynchronize(tst_));
+  int one = 1;
+  std::vector<int> all(world_);
+  if (td_status e = allgather(&one, all.data(), sizeof one)) return e;
+  for (auto& kv : peer_mbox_) cudaIpcCloseMemHandle(kv.second);
+  peer_mbox_.clear();
+  cudaFree(mbox_);
+  mbox_ = nullptr;
+  return TD_OK;
 }
 
 // ------------------------------------------------------------------ factory

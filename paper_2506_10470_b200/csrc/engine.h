@@ -29,6 +29,15 @@ struct KernelTiming {
   double flops = 0.0;
 };
 
+// One (micro-batch, stage) span of a timed td_run, ns from the run's first
+// launch (CUDA events on the library stream), for td_write_trace.
+struct TraceSpan {
+  int64_t mid;
+  char kind;
+  int stage;
+  int64_t a_ns, b_ns;
+};
+
 class Engine : public ExecHooks {
  public:
   virtual ~Engine() {}
@@ -50,6 +59,11 @@ class Engine : public ExecHooks {
                             std::vector<int64_t>* tpre) = 0;
   // logical [rows, cols] bf16 bits of F9 tensor `tid` (td_get_weight)
   virtual td_status get_weight(int tid, std::vector<uint16_t>* out, int64_t* rows, int64_t* cols) = 0;
+  // td_bench_step: one synthetic micro-batch of this process's stages, timed
+  // per kernel class (accumulators readable through get_timing)
+  virtual td_status bench_step(bool prefill, int n, int len, int iters, double* step_ms, double* ideal_ms) = 0;
+  // spans and (time ns, KV blocks in use) samples of the last timed td_run
+  virtual void get_trace(std::vector<TraceSpan>* spans, std::vector<std::pair<int64_t, int64_t>>* kv) = 0;
   virtual void set_timing(bool on) = 0;
   virtual bool get_timing(const std::string& name, KernelTiming* t) = 0;
   std::string error;

@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -153,6 +155,80 @@ __device__ __forceinline__ void attn_finish(const DecodeAttnParams& p, int seq, 
 }
 
 
+
+// Fused QKV split-K epilogue of the tensor-core kernel's q-prep warp (the SIMT
+// kernel inlines the same arithmetic): q of the G heads of kv head kh, plus
+// k / v of the newest token when `has_new`; partials summed in split order,
+// RoPE at position `newest` on the interleaved (i, i+hd/2) pairs, bf16 -- bit
+// for bit the arithmetic of splitk_reduce_kernel.  s_qkv = [q_0 .. q_{G-1},
+// k, v] x HD.
+template <int HD, int G, int NBT>
+TDP_DEV void fused_qkv_reduce(const DecodeAttnParams& p, int seq, int kh, int newest, bool has_new, bf16* s_qkv,
+                              int tid, int nthr) {
+  // NBT pairs per thread per round: all their split partials are loaded
+  // before any is summed (NBT x 8 float2 in flight per thread)
+  const int H = p.H;
+  const int npairs = (G + (has_new ? 2 : 0)) * (HD / 2);
+  for (int p0 = tid; p0 < npairs; p0 += nthr * NBT) {
+    float2 pr[NBT][8];
+    int fs[NBT];
+    bool rp[NBT];
+#pragma unroll
+    for (int u = 0; u < NBT; ++u) {
+      const int e = (p0 + u * nthr) * 2;
+      int f = 0;
+      bool rope = true;
+      if (e < G * HD) f = kh * G * HD + e;
+      else if (e < (G + 1) * HD) f = (H + kh) * HD + (e - G * HD);
+      else { f = (H + p.Hkv + kh) * HD + (e - (G + 1) * HD); rope = false; }
+      fs[u] = f;
+      rp[u] = rope;
+      const bool ok = p0 + u * nthr < npairs;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+        if (ok && s2 < p.qkv_splits)
+          pr[u][s2] = __ldcg(reinterpret_cast<const float2*>(p.qkv_ws + ((int64_t)s2 * p.n + seq) * p.nqkv + f));
+    }
+#pragma unroll
+    for (int u = 0; u < NBT; ++u) {
+      if (p0 + u * nthr >= npairs) break;
+      const int e = (p0 + u * nthr) * 2, f = fs[u];
+      const float2 cs = rp[u] ? *reinterpret_cast<const float2*>(p.rope_cs + ((int64_t)newest * (HD >> 1) + ((f % HD) >> 1)) * 2)
+                              : make_float2(1.f, 0.f);
+      float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+        if (s2 < p.qkv_splits) { v0 += pr[u][s2].x; v1 += pr[u][s2].y; }
+      for (int s2 = 8; s2 < p.qkv_splits; ++s2) {
+        const float2 q2 = __ldcg(reinterpret_cast<const float2*>(p.qkv_ws + ((int64_t)s2 * p.n + seq) * p.nqkv + f));
+        v0 += q2.x;
+        v1 += q2.y;
+      }
+      float r0 = v0, r1 = v1;
+      if (rp[u]) {
+        r0 = v0 * cs.x - v1 * cs.y;
+        r1 = v1 * cs.x + v0 * cs.y;
+      }
+      *reinterpret_cast<uint32_t*>(s_qkv + e) = pack_bf16x2(r0, r1);
+    }
+  }
+}
+
+// The newest token's K / V (s_qkv[G], s_qkv[G+1]) into its paged-cache slot:
+// threads tid < HD/8 store one 16-byte chunk of each (after a barrier that
+// follows fused_qkv_reduce).
+template <int HD, int G>
+TDP_DEV void store_new_kv(const DecodeAttnParams& p, int seq, int kh, int newest, const bf16* s_qkv, int tid) {
+  if (tid >= HD / 8) return;
+  const int64_t head_stride = (int64_t)kBlock * HD;
+  const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
+  const int64_t kb = (((int64_t)bt[newest >> 4] * 2) * p.Hkv + kh) * head_stride + (newest & 15) * HD + tid * 8;
+  bf16* kvw = const_cast<bf16*>(p.kv);
+  *reinterpret_cast<uint4*>(kvw + kb) = *reinterpret_cast<const uint4*>(s_qkv + G * HD + tid * 8);
+  *reinterpret_cast<uint4*>(kvw + kb + (int64_t)p.Hkv * head_stride) =
+      *reinterpret_cast<const uint4*>(s_qkv + (G + 1) * HD + tid * 8);
+}
+
 // One CTA attends (sequence seq, kv head kh) over context tokens
 // [t_begin, t_end): segment `split` of `n_splits`.  With n_splits == 1 it writes
 // o; otherwise it writes the segment's partial (m, l, acc) and the last
@@ -214,10 +290,6 @@ __device__ __forceinline__ void attend_range(const DecodeAttnParams& p, int seq,
   pdl_wait();
   __shared__ __align__(16) bf16 s_qkv[(G + 2) * HD];
   if (fused) {
-    // the QKV split-K epilogue, done cooperatively (all loads in flight at
-    // once): q of the G heads of kv head kh, plus k / v of the newest token
-    // when this CTA holds it; sum in split order, RoPE at position ctx-1 on
-    // the interleaved (i, i+hd/2) pairs, bf16 -- as splitk_reduce_kernel
     const int npairs = (G + (has_new ? 2 : 0)) * (HD / 2);
     for (int pi = threadIdx.x; pi < npairs; pi += NW * 32) {
       const int e = pi * 2;
@@ -361,252 +433,598 @@ decode_attn_kernel(DecodeAttnParams p) {
   attend_range<HD, G>(p, seq, kh, t_begin, min(ctx, t_begin + len), split, n_splits, ctx - 1);
 }
 
-// ---------------------------------------------------------------- decode v2
-// Page-streaming variant: a producer warp copies whole K and V pages (16 tokens
-// x hd, contiguous in the paged pool) into an R-slot shared-memory ring with
-// cp.async.bulk + mbarrier transaction counts; 4 consumer warps each own every
-// 4th page and compute scores / online softmax / PV from shared memory.  The
-// in-flight bytes live in smem rather than registers, so a few CTAs per SM keep
-// enough of HBM busy even for small batches with long contexts.
+// ------------------------------------------------------ decode, tensor cores
+// GQA decode attention on tensor cores (G = H/Hkv query heads share each K/V
+// page; Table 2's 32B / 70B models are GQA).  One CTA per
+// (split, kv head, sequence), as the SIMT kernel, but:
+//  * a producer warp streams the split's 16-token K and V pages with TMA
+//    (cp.async.bulk.tensor, 128B-swizzled 64-column boxes, L2 evict-first)
+//    into an R-slot shared-memory ring (mbarrier transaction counts), so a CTA
+//    keeps R x 8 KB in flight without holding it in registers;
+//  * 4 consumer warps each take every 4th page (slot = page mod R, R a
+//    multiple of 4: one consumer per slot, never two phases ahead) and compute
+//    transposed tiles on mma.sync m16n8k16 (bf16 in, fp32 accumulate):
+//      S^T[16 tokens x 8 heads]  = K[16 x hd] . Q^T[hd x 8]       (8 HMMA)
+//      O^T[hd x 8 heads]        += V^T[hd x 16] . P^T[16 x 8]      (8 HMMA)
+//    with the G <= 8 heads as the n = 8 dimension (no padding for G = 8);
+//    K is the row-major A operand (ldmatrix), V^T comes from ldmatrix.trans,
+//    and P^T is the exp2'd S^T accumulator transposed in registers with
+//    movmatrix (the C layout of S^T is the B layout of P^T after an 8x8
+//    transpose), so P never touches shared memory;
+//  * online softmax per head (a column of S^T): column max over the 16 tokens
+//    with 3 shuffles, per-thread partial sums reduced once at the end;
+//  * warps merge through shared memory, then the split merge of the SIMT
+//    kernel (partials in split order, last CTA merges).
+// The newest token of a fused-QKV decode step is not in the cache yet: it is
+// left out of the streamed range and added in the merge (as the SIMT kernel).
 namespace {
-TDP_DEV void dmbar_init(uint64_t* b, uint32_t c) {
+TDP_DEV void tc_mbar_init(uint64_t* b, uint32_t c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
 }
-TDP_DEV void dmbar_wait(uint64_t* b, uint32_t parity) {
+TDP_DEV void tc_mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   while (!done)
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
                  : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
 }
-TDP_DEV void dmbar_arrive(uint64_t* b) {
+TDP_DEV void tc_mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-TDP_DEV void dmbar_expect(uint64_t* b, uint32_t bytes) {
+TDP_DEV void tc_mbar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
-TDP_DEV void dbulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+TDP_DEV void tma_load_3d_ef(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
+TDP_DEV void ldsm4(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+TDP_DEV void ldsm4_t(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+TDP_DEV uint32_t movm_t(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+TDP_DEV void hmma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// byte offset of (row r, 16-byte chunk ch) in a page staged as hd/64 boxes of
+// [16 rows][128 B] with the 128B swizzle (chunk ^ (row & 7))
+TDP_DEV uint32_t page_off(int r, int ch) { return (uint32_t)((ch >> 3) * 2048 + r * 128 + (((ch & 7) ^ (r & 7)) << 4)); }
 }  // namespace
 
-template <int HD, int G, int RW>
-__global__ void __launch_bounds__(160)
-decode_attn_v2_kernel(DecodeAttnParams p) {
-  constexpr int LPT = HD / 8, TPW = 32 / LPT, NWC = 4;
-  constexpr int R = NWC * RW;                      // ring slots (RW per consumer warp)
-  constexpr int PAGE = kBlock * HD * 2;            // bytes of one K (or V) page
-  extern __shared__ __align__(128) uint8_t dsm[];
-  uint8_t* ring = dsm;                             // R x (K page, V page)
-  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + R * 2 * PAGE);
-  uint64_t* empty = full + R;
-  float* sm = reinterpret_cast<float*>(empty + R);            // [NWC][G][2]
-  float* sacc = sm + NWC * G * 2;                             // [NWC][G][HD]
-  __shared__ int s_last;
+constexpr int kTcRing = 8;          // page ring slots (a multiple of the 4 consumer warps)
+constexpr int kTcItemQ = 3;         // work items in flight per CTA (queue slots)
+constexpr int kTcThreads = 224;     // 4 consumer warps, producer, q-prep, merger
+constexpr int kTcPad = 4;           // sO row padding (floats): conflict-free fragment stores
+constexpr int kTcMaxSplits = 32;    // split merge weights held in shared memory
 
-  pdl_trigger();
-  const int seq = blockIdx.z, kh = blockIdx.y, split = blockIdx.x;
-  const int ctx = p.ctx[seq];
-  const int n_splits = (ctx + p.split_tokens - 1) / p.split_tokens;
-  if (split >= n_splits) return;
-  const int t_begin = split * p.split_tokens;
-  const int t_end = min(ctx, t_begin + p.split_tokens);
-  const int pg0 = t_begin >> 4, npg = ((t_end + 15) >> 4) - pg0;
+// Shared-memory layout of decode_attn_tc_kernel (dynamic part), in bytes.
+template <int HD, int G>
+struct TcLayout {
+  static constexpr int PAGE = kBlock * HD * 2;                 // one K (or V) page
+  static constexpr int SLOT = 2 * PAGE;
+  static constexpr int RING = kTcRing * SLOT;
+  static constexpr int OBUF = 4 * (G * (HD + kTcPad) + 2 * 8) * 4;   // 4 warps: O^T rows, then m[8], l[8]
+  static constexpr int QBUF = (G + 2) * HD * 2;                // q of G heads, newest k, v
+  static constexpr int BARS = (2 * kTcRing + 3 * kTcItemQ + 4) * 8;
+  static constexpr int FIXED = RING + 2 * OBUF + kTcItemQ * QBUF + BARS + 1024;   // + alignment
+  static int bytes(int n) { return FIXED + (n + 1) * 4; }
+};
+
+// Persistent, warp-specialised pipeline.  Work items are (sequence, split,
+// kv head), numbered sequence-major over the non-empty splits; a CTA takes
+// items from an atomic counter until they run out:
+//   producer  (warp 4): fetches item indices into a kTcItemQ-slot queue and
+//             streams each item's K / V pages into the page ring by TMA
+//             (block-table entries read 32 at a time by the whole warp);
+//   q-prep    (warp 5): for each queued item stages q of its G heads in
+//             shared memory (one bulk copy, or the fused QKV split-K reduce +
+//             RoPE, which also writes the newest token's K / V to the cache);
+//   consumers (warps 0-3): per item, tensor-core S^T / online softmax / O^T
+//             over every 4th page, then their (m, l, O) into one of two
+//             result buffers;
+//   merger    (warp 6): combines the 4 warps (+ the newest token of a fused
+//             step), writes o or the split partial, and the last split of a
+//             (sequence, kv head) merges all partials in split order.
+// So q loads, merges and split merges of one item overlap the page streaming
+// of the next.  Local page j of an item always goes to consumer warp j mod 4
+// (only the ring slot -- one of that warp's own slots -- depends on the CTA's
+// history), so each item is computed identically whichever CTA takes it:
+// results are bitwise reproducible.
+template <int HD, int G>
+__global__ void __launch_bounds__(kTcThreads, 2)
+decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParams p) {
+  using Lay = TcLayout<HD, G>;
+  constexpr int NWC = 4, R = kTcRing, Q = kTcItemQ;
+  constexpr int PAGE = Lay::PAGE, SLOT = Lay::SLOT;
+  constexpr int NB = HD / 64;                    // 64-column TMA boxes per page
+  constexpr int KS = HD / 16;                    // k-steps of S^T / m-tiles of O^T
+  constexpr int OS = HD + kTcPad;                // sO row stride (floats)
+  constexpr int RW = R / 4;                      // ring slots per consumer warp
+  static_assert(G >= 1 && G <= 8 && R % NWC == 0, "layout");
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  float* obuf = reinterpret_cast<float*>(ring + Lay::RING);                  // [2][OBUF]
+  bf16* qbuf = reinterpret_cast<bf16*>(ring + Lay::RING + 2 * Lay::OBUF);  // [Q][(G+2) HD]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + Lay::RING + 2 * Lay::OBUF + Q * Lay::QBUF);
+  uint64_t* empty = full + R;
+  uint64_t* ifull = empty + R;     // item queued (producer)
+  uint64_t* qready = ifull + Q;    // its q staged (q-prep)
+  uint64_t* iempty = qready + Q;   // its slot free again (merger)
+  uint64_t* oready = iempty + Q;   // [2] result buffer written (4 consumer warps)
+  uint64_t* ofree = oready + 2;    // [2] result buffer read (merger)
+  int* pfx = reinterpret_cast<int*>(ofree + 2);                      // [n + 1] split prefix sums
+  __shared__ int s_item[Q];
+  __shared__ float s_c[G][kTcMaxSplits];   // merger: split (m, then weights) and l
+  __shared__ float s_l[G][kTcMaxSplits];
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = p.H;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < R; ++i) {
-      dmbar_init(&full[i], 1);
-      dmbar_init(&empty[i], 1);
+  const bool fused = p.qkv_ws != nullptr;
+  const float scale = rsqrtf((float)HD) * kLog2e;
+  struct Item {
+    int seq, kh, split, n_splits, t_begin, t_end, pg0, npg;
+    bool has_new;
+  };
+  // item idx = (pfx[seq] + split) * Hkv + kh; streamed range [t_begin, t_end)
+  // excludes the newest token of a fused-QKV step (not in the cache yet)
+  auto item_of = [&](int idx) {
+    Item it;
+    const int u = idx / p.Hkv;
+    it.kh = idx - u * p.Hkv;
+    int lo = 0, hi = p.n - 1;   // last seq with pfx[seq] <= u
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pfx[mid] <= u) lo = mid;
+      else hi = mid - 1;
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    it.seq = lo;
+    it.split = u - pfx[lo];
+    it.n_splits = pfx[lo + 1] - pfx[lo];
+    const int ctx = p.ctx[it.seq];
+    it.t_begin = it.split * p.split_tokens;
+    it.t_end = min(ctx, it.t_begin + p.split_tokens);
+    it.has_new = fused && ctx - 1 >= it.t_begin && ctx - 1 < it.t_end;
+    if (it.has_new) it.t_end = ctx - 1;
+    it.pg0 = it.t_begin >> 4;
+    it.npg = it.t_end > it.t_begin ? ((it.t_end + 15) >> 4) - it.pg0 : 0;
+    return it;
+  };
+  {   // pfx[i] = sum_{j < i} ceil(ctx[j] / split_tokens): contiguous chunks + a block scan
+    __shared__ int s_wsum[kTcThreads / 32];
+    const int per = (p.n + kTcThreads - 1) / kTcThreads;
+    const int i0 = min(p.n, (int)threadIdx.x * per), i1 = min(p.n, i0 + per);
+    int sum = 0;
+    for (int i = i0; i < i1; ++i) sum += (p.ctx[i] + p.split_tokens - 1) / p.split_tokens;
+    int incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    if (threadIdx.x == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+      for (int i = 0; i < R; ++i) {
+        tc_mbar_init(&full[i], 1);
+        tc_mbar_init(&empty[i], 1);
+      }
+      for (int i = 0; i < Q; ++i) {
+        tc_mbar_init(&ifull[i], 1);
+        tc_mbar_init(&qready[i], 1);
+        tc_mbar_init(&iempty[i], 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        tc_mbar_init(&oready[i], NWC);
+        tc_mbar_init(&ofree[i], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp; ++w) base += s_wsum[w];
+    int run = base + incl - sum;
+    for (int i = i0; i < i1; ++i) {
+      pfx[i] = run;
+      run += (p.ctx[i] + p.split_tokens - 1) / p.split_tokens;
+    }
+    if (threadIdx.x == kTcThreads - 1) pfx[p.n] = run;
   }
   __syncthreads();
+  const int n_items = pfx[p.n] * p.Hkv;
+  // Every K / V page was written before this kernel started (this step's QKV
+  // epilogue writes only the newest token, which a fused step handles in the
+  // merge); nothing is read before the wait.
   pdl_wait();
-  const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
-  const int64_t head_stride = (int64_t)kBlock * HD;
 
-  if (warp == NWC) {   // producer
-    if (lane == 0) {
-      // page i belongs to consumer warp i % NWC, which owns slots
-      // [w*RW, (w+1)*RW) and consumes them strictly in order (one consumer per
-      // barrier: a parity wait can never be two phases ahead)
-      for (int i = 0; i < npg; ++i) {
-        const int w = i % NWC, j = i / NWC;
-        const int s = w * RW + j % RW;
-        if (j >= RW) dmbar_wait(&empty[s], ((j / RW) & 1) ^ 1);
-        const int blk = bt[pg0 + i];
-        const bf16* kp = p.kv + (((int64_t)blk * 2) * p.Hkv + kh) * head_stride;
-        dmbar_expect(&full[s], 2 * PAGE);
-        dbulk(ring + s * 2 * PAGE, kp, PAGE, &full[s]);
-        dbulk(ring + s * 2 * PAGE + PAGE, kp + (int64_t)p.Hkv * head_stride, PAGE, &full[s]);
+  if (warp == NWC) {   // ---------------------------------------------------- producer
+    // Page j of an item goes to consumer warp j mod 4 and into one of that
+    // warp's own ring slots (w, w + 4, ...): every slot has exactly one
+    // consumer, which takes its pages in order, so a parity wait is never two
+    // phases ahead even though the warps run items out of step.
+    const uint64_t pol = l2_evict_first_policy();
+    int c0 = 0, c1 = 0, c2 = 0, c3 = 0;   // pages issued per consumer warp
+    int next = 0;
+    if (lane == 0) next = atomicAdd(p.work, 1);
+    next = __shfl_sync(0xffffffffu, next, 0);
+    for (int n = 0;; ++n) {
+      const int idx = next < n_items ? next : -1;
+      const int q = n % Q;
+      if (n >= Q) tc_mbar_wait(&iempty[q], ((uint32_t)(n / Q) & 1u) ^ 1u);
+      if (lane == 0) {
+        s_item[q] = idx;
+        tc_mbar_arrive(&ifull[q]);
+        if (idx >= 0) next = atomicAdd(p.work, 1);
+        else pdl_trigger();   // no work left for this CTA: the next kernel may start its prologue
       }
-    }
-  } else {
-    const int tg = lane / LPT, sub = lane % LPT;
-    const float scale = rsqrtf((float)HD) * kLog2e;
-    float q[G][8], m[G], l[G], acc[G][8];
+      if (idx < 0) break;
+      const Item it = item_of(idx);
+      const int32_t* bt = p.bt + (int64_t)it.seq * p.maxblk + it.pg0;
+      for (int j0 = 0; j0 < it.npg; j0 += 32) {
+        const int btv = j0 + lane < it.npg ? __ldg(bt + j0 + lane) : 0;
+        const int cn = min(32, it.npg - j0);
+        for (int j = 0; j < cn; ++j) {
+          const int blk = __shfl_sync(0xffffffffu, btv, j);
+          const int w = (j0 + j) & 3;
+          int& cw = w == 0 ? c0 : w == 1 ? c1 : w == 2 ? c2 : c3;
+          const int s = w + NWC * (cw % RW), use = cw / RW;
+          ++cw;
+          if (use > 0) tc_mbar_wait(&empty[s], ((uint32_t)use & 1u) ^ 1u);
+          if (lane == 0) {
+            const int row = ((blk * 2) * p.Hkv + it.kh) * kBlock;
+            uint8_t* dst = ring + s * SLOT;
+            tc_mbar_expect(&full[s], SLOT);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const uint4 u = *reinterpret_cast<const uint4*>(p.q + ((int64_t)seq * H + kh * G + g) * HD + sub * 8);
-      bf16x8_to_f32(u, q[g]);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) q[g][i] *= scale;
-      m[g] = -INFINITY;
-      l[g] = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
-    }
-    for (int i = warp; i < npg; i += NWC) {
-      const int j = i / NWC;
-      const int s = warp * RW + j % RW;
-      dmbar_wait(&full[s], (j / RW) & 1);
-      const uint8_t* kpg = ring + s * 2 * PAGE;
-      const uint8_t* vpg = kpg + PAGE;
-      const int tbase = (pg0 + i) << 4;
-#pragma unroll
-      for (int it = 0; it < kBlock / TPW; ++it) {
-        const int r = it * TPW + tg;                 // token row inside the page
-        const bool valid = tbase + r < t_end;
-        float kf[8], vf[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(kpg + (r * HD + sub * 8) * 2), kf);
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(vpg + (r * HD + sub * 8) * 2), vf);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          float sc = 0.f;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) sc = fmaf(q[g][k], kf[k], sc);
-#pragma unroll
-          for (int o = LPT / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-          if (valid) {
-            const float mn = fmaxf(m[g], sc);
-            const float corr = exp2f(m[g] - mn);
-            const float pr = exp2f(sc - mn);
-            l[g] = l[g] * corr + pr;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[g][k] = fmaf(pr, vf[k], acc[g][k] * corr);
-            m[g] = mn;
+            for (int b = 0; b < NB; ++b) {
+              tma_load_3d_ef(dst + b * 2048, &kvmap, b * 64, row, p.layer, &full[s], pol);
+              tma_load_3d_ef(dst + PAGE + b * 2048, &kvmap, b * 64, row + p.Hkv * kBlock, p.layer, &full[s], pol);
+            }
           }
         }
       }
+      next = __shfl_sync(0xffffffffu, next, 0);
+    }
+  } else if (warp == NWC + 1) {   // ------------------------------------------ q-prep
+    for (int n = 0;; ++n) {
+      const int q = n % Q;
+      tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u);
+      const int idx = s_item[q];
+      bf16* sq = qbuf + q * (G + 2) * HD;
+      if (idx < 0) {
+        if (lane == 0) tc_mbar_arrive(&qready[q]);
+        break;
+      }
+      const Item it = item_of(idx);
+      if (fused) {
+        fused_qkv_reduce<HD, G, 4>(p, it.seq, it.kh, p.ctx[it.seq] - 1, it.has_new, sq, lane, 32);
+        __syncwarp();
+        if (it.has_new) store_new_kv<HD, G>(p, it.seq, it.kh, p.ctx[it.seq] - 1, sq, lane);
+        __syncwarp();
+        if (lane == 0) tc_mbar_arrive(&qready[q]);
+      } else if (lane == 0) {
+        tc_mbar_expect(&qready[q], G * HD * 2);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sq)),
+            "l"(p.q + ((int64_t)it.seq * H + it.kh * G) * HD), "r"(G * HD * 2), "r"(smem_u32(&qready[q]))
+            : "memory");
+      }
+    }
+  } else if (warp == NWC + 2) {   // ------------------------------------------ merger
+    for (int n = 0;; ++n) {
+      const int q = n % Q, b = n & 1;
+      tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u);
+      const int idx = s_item[q];
+      if (idx < 0) break;
+      const Item it = item_of(idx);
+      const bf16* sq = qbuf + q * (G + 2) * HD;
+      tc_mbar_wait(&oready[b], (uint32_t)(n >> 1) & 1u);
+      const float* so = obuf + b * (Lay::OBUF / 4);
+      const float* sm = so + NWC * G * OS;      // [4][8]
+      const float* sl = sm + NWC * 8;           // [4][8]
+      float A[G][HD / 32], Mg[G], Lg[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NWC; ++w) M = fmaxf(M, sm[w * 8 + g]);
+        float c[NWC], L = 0.f;
+#pragma unroll
+        for (int w = 0; w < NWC; ++w) {
+          c[w] = sm[w * 8 + g] == -INFINITY ? 0.f : exp2f(sm[w * 8 + g] - M);
+          L += sl[w * 8 + g] * c[w];
+        }
+#pragma unroll
+        for (int dd = 0; dd < HD / 32; ++dd) {
+          float a = 0.f;
+#pragma unroll
+          for (int w = 0; w < NWC; ++w) a += so[(w * G + g) * OS + dd * 32 + lane] * c[w];
+          A[g][dd] = a;
+        }
+        if (it.has_new) {   // the newest token (not streamed): score, then one online-softmax step
+          float sn = 0.f;
+          for (int e = lane; e < HD; e += 32) sn += __bfloat162float(sq[g * HD + e]) * __bfloat162float(sq[G * HD + e]);
+          sn = warp_sum(sn) * scale;
+          const float Mn = fmaxf(M, sn);
+          const float cm = M == -INFINITY ? 0.f : exp2f(M - Mn);
+          const float pn = exp2f(sn - Mn);
+          L = L * cm + pn;
+#pragma unroll
+          for (int dd = 0; dd < HD / 32; ++dd)
+            A[g][dd] = A[g][dd] * cm + pn * __bfloat162float(sq[(G + 1) * HD + dd * 32 + lane]);
+          M = Mn;
+        }
+        Mg[g] = M;
+        Lg[g] = L;
+      }
+      const Item itc = it;
       __syncwarp();
-      if (lane == 0) dmbar_arrive(&empty[s]);
-    }
-    // merge the token groups of the warp, then the warps through smem
-#pragma unroll
-    for (int o = LPT; o < 32; o <<= 1) {
+      if (lane == 0) {
+        tc_mbar_arrive(&ofree[b]);   // the consumers may reuse result buffer b
+        tc_mbar_arrive(&iempty[q]);  // queue slot q (descriptor, q buffer) free: the results are in registers
+      }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m[g], o);
-        const float l2 = __shfl_xor_sync(0xffffffffu, l[g], o);
-        const float mn = fmaxf(m[g], m2);
-        const float c1 = mn == -INFINITY ? 0.f : exp2f(m[g] - mn);
-        const float c2 = mn == -INFINITY ? 0.f : exp2f(m2 - mn);
-        l[g] = l[g] * c1 + l2 * c2;
+        const int h = itc.kh * G + g;
+        if (itc.n_splits == 1) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float a2 = __shfl_xor_sync(0xffffffffu, acc[g][k], o);
-          acc[g][k] = acc[g][k] * c1 + a2 * c2;
+          for (int dd = 0; dd < HD / 32; ++dd)
+            p.o[((int64_t)itc.seq * H + h) * HD + dd * 32 + lane] = __float2bfloat16_rn(A[g][dd] / Lg[g]);
+        } else {
+          float* part = p.part + (((int64_t)itc.seq * H + h) * p.max_splits + itc.split) * (HD + 2);
+#pragma unroll
+          for (int dd = 0; dd < HD / 32; ++dd) __stcg(part + 2 + dd * 32 + lane, A[g][dd]);
+          if (lane == 0) {
+            __stcg(part, Mg[g]);
+            __stcg(part + 1, Lg[g]);
+          }
         }
-        m[g] = mn;
       }
-    }
-    if (tg == 0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (sub == 0) {
-          sm[(warp * G + g) * 2] = m[g];
-          sm[(warp * G + g) * 2 + 1] = l[g];
+      if (itc.n_splits > 1) {
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          __threadfence();
+          last = atomicAdd(&p.counters[itc.seq * p.Hkv + itc.kh], 1) == itc.n_splits - 1;
         }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {   // merge every split's partial of the G heads, in split order
+          __threadfence();
+          const int ns = itc.n_splits;
+          const float* part0 = p.part + ((int64_t)itc.seq * H + itc.kh * G) * p.max_splits * (HD + 2);
+          // (m, l) of every (head, split) in one round trip, staged in shared memory
+          for (int e = lane; e < G * ns; e += 32) {
+            const int g = e / ns, s2 = e - g * ns;
+            const float* ps = part0 + ((int64_t)g * p.max_splits + s2) * (HD + 2);
+            s_c[g][s2] = __ldcg(ps);
+            s_l[g][s2] = __ldcg(ps + 1);
+          }
+          __syncwarp();
+          float Lh[G];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) sacc[(warp * G + g) * HD + sub * 8 + k] = acc[g][k];
+          for (int g = 0; g < G; ++g) {   // weights c = exp2(m - M), in split order (every lane the same)
+            float M = -INFINITY;
+            for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, s_c[g][s2]);
+            float L = 0.f;
+            for (int s2 = 0; s2 < ns; ++s2) L += s_l[g][s2] * exp2f(s_c[g][s2] - M);
+            Lh[g] = L;
+            __syncwarp();
+            for (int s2 = lane; s2 < ns; s2 += 32) s_c[g][s2] = exp2f(s_c[g][s2] - M);
+            __syncwarp();
+          }
+          float acc[G][HD / 32];
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int dd = 0; dd < HD / 32; ++dd) acc[g][dd] = 0.f;
+          for (int s2 = 0; s2 < ns; s2 += 2) {   // split order; 2 splits x G x HD/32 loads in flight
+            float v0[G][HD / 32], v1[G][HD / 32];
+            const bool two = s2 + 1 < ns;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float* ps = part0 + ((int64_t)g * p.max_splits + s2) * (HD + 2) + 2;
+#pragma unroll
+              for (int dd = 0; dd < HD / 32; ++dd) {
+                v0[g][dd] = __ldcg(ps + dd * 32 + lane);
+                v1[g][dd] = two ? __ldcg(ps + (HD + 2) + dd * 32 + lane) : 0.f;
+              }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float c0 = s_c[g][s2], c1 = two ? s_c[g][s2 + 1] : 0.f;
+#pragma unroll
+              for (int dd = 0; dd < HD / 32; ++dd) acc[g][dd] = acc[g][dd] + c0 * v0[g][dd] + c1 * v1[g][dd];
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float inv = 1.f / Lh[g];
+#pragma unroll
+            for (int dd = 0; dd < HD / 32; ++dd)
+              p.o[((int64_t)itc.seq * H + itc.kh * G + g) * HD + dd * 32 + lane] = __float2bfloat16_rn(acc[g][dd] * inv);
+          }
+          __syncwarp();
+          if (lane == 0) p.counters[itc.seq * p.Hkv + itc.kh] = 0;
+        }
       }
     }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
-    const int g = e / HD, dim = e % HD;
-    float M = -INFINITY;
+  } else {             // ---------------------------------------------------- consumers
+    const int g = lane >> 2, t4 = lane & 3;
+    const int mi = lane >> 3, rr = lane & 7;
+    const int k_row = rr + 8 * (mi & 1), k_ch = mi >> 1;    // K: A operand, row-major
+    const int v_row = rr + 8 * (mi >> 1), v_ch = mi & 1;    // V^T: A operand via .trans
+    int cw = 0;   // pages this warp has taken (its slots: warp, warp + 4, ...)
+    for (int n = 0;; ++n) {
+      const int q = n % Q, b = n & 1;
+      tc_mbar_wait(&qready[q], (uint32_t)(n / Q) & 1u);
+      const int idx = s_item[q];
+      if (idx < 0) break;
+      const Item it = item_of(idx);
+      const bf16* sq = qbuf + q * (G + 2) * HD;
+      // Q^T as the B operand of S^T = K Q^T: b0 = Q[head g][16j + 2t4 ..], b1 = [.. + 8]
+      uint32_t qb[KS][2];
 #pragma unroll
-    for (int w = 0; w < NWC; ++w) M = fmaxf(M, sm[(w * G + g) * 2]);
-    float L = 0.f, A = 0.f;
-#pragma unroll
-    for (int w = 0; w < NWC; ++w) {
-      const float c = M == -INFINITY ? 0.f : exp2f(sm[(w * G + g) * 2] - M);
-      L += sm[(w * G + g) * 2 + 1] * c;
-      A += sacc[(w * G + g) * HD + dim] * c;
-    }
-    const int h = kh * G + g;
-    if (n_splits == 1) {
-      p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
-    } else {
-      float* part = p.part + (((int64_t)seq * H + h) * p.max_splits + split) * (HD + 2);
-      __stcg(part + 2 + dim, A);
-      if (dim == 0) {
-        __stcg(part, M);
-        __stcg(part + 1, L);
+      for (int j = 0; j < KS; ++j) {
+        qb[j][0] = g < G ? *reinterpret_cast<const uint32_t*>(sq + g * HD + 16 * j + 2 * t4) : 0u;
+        qb[j][1] = g < G ? *reinterpret_cast<const uint32_t*>(sq + g * HD + 16 * j + 8 + 2 * t4) : 0u;
       }
+      float o[KS][4];
+#pragma unroll
+      for (int i = 0; i < KS; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // heads 2t4, 2t4+1
+      for (int j = warp; j < it.npg; j += NWC, ++cw) {
+        const int s = warp + NWC * (cw % RW);
+        tc_mbar_wait(&full[s], (uint32_t)(cw / RW) & 1u);
+        const uint32_t kt = smem_u32(ring + s * SLOT), vt = kt + PAGE;
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int jj = 0; jj < KS; ++jj) {
+          uint32_t a[4];
+          ldsm4(a, kt + page_off(k_row, 2 * jj + k_ch));
+          hmma16816(sc, a, qb[jj][0], qb[jj][1]);
+        }
+        const int tb = (it.pg0 + j) << 4;
+        const bool ok0 = tb + g < it.t_end, ok1 = tb + g + 8 < it.t_end;
+        const float x0 = ok0 ? sc[0] * scale : -INFINITY, x1 = ok0 ? sc[1] * scale : -INFINITY;
+        const float x2 = ok1 ? sc[2] * scale : -INFINITY, x3 = ok1 ? sc[3] * scale : -INFINITY;
+        float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);   // finite: every page holds >= 1 valid token
+        const float c0 = exp2f(m0 - mn0), c1 = exp2f(m1 - mn1);
+        const float p0 = exp2f(x0 - mn0), p1 = exp2f(x1 - mn1), p2 = exp2f(x2 - mn0), p3 = exp2f(x3 - mn1);
+        l0 = l0 * c0 + (p0 + p2);
+        l1 = l1 * c1 + (p1 + p3);
+        m0 = mn0;
+        m1 = mn1;
+        const uint32_t b0 = movm_t(pack_bf16x2(p0, p1)), b1 = movm_t(pack_bf16x2(p2, p3));
+#pragma unroll
+        for (int d = 0; d < KS; ++d) {
+          o[d][0] *= c0;
+          o[d][1] *= c1;
+          o[d][2] *= c0;
+          o[d][3] *= c1;
+          uint32_t a[4];
+          ldsm4_t(a, vt + page_off(v_row, 2 * d + v_ch));
+          hmma16816(o[d], a, b0, b1);
+        }
+        __syncwarp();
+        if (lane == 0) tc_mbar_arrive(&empty[s]);
+      }
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+      }
+      if (n >= 2) tc_mbar_wait(&ofree[b], ((uint32_t)(n >> 1) & 1u) ^ 1u);
+      float* so = obuf + b * (Lay::OBUF / 4);
+      float* sm = so + NWC * G * OS;
+      float* sl = sm + NWC * 8;
+      if (g == 0) {
+        if (2 * t4 < G) { sm[warp * 8 + 2 * t4] = m0; sl[warp * 8 + 2 * t4] = l0; }
+        if (2 * t4 + 1 < G) { sm[warp * 8 + 2 * t4 + 1] = m1; sl[warp * 8 + 2 * t4 + 1] = l1; }
+      }
+#pragma unroll
+      for (int d = 0; d < KS; ++d) {
+        const int h0 = 2 * t4, h1 = 2 * t4 + 1, r0 = 16 * d + g;
+        if (h0 < G) {
+          so[(warp * G + h0) * OS + r0] = o[d][0];
+          so[(warp * G + h0) * OS + r0 + 8] = o[d][2];
+        }
+        if (h1 < G) {
+          so[(warp * G + h1) * OS + r0] = o[d][1];
+          so[(warp * G + h1) * OS + r0 + 8] = o[d][3];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc_mbar_arrive(&oready[b]);
     }
   }
-  if (n_splits == 1) return;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[seq * p.Hkv + kh], 1) == n_splits - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
-    const int g = e / HD, dim = e % HD;
-    const int h = kh * G + g;
-    const float* part = p.part + ((int64_t)seq * H + h) * p.max_splits * (HD + 2);
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < n_splits; ++s2) M = fmaxf(M, __ldcg(part + s2 * (HD + 2)));
-    float L = 0.f, A = 0.f;
-    for (int s2 = 0; s2 < n_splits; ++s2) {
-      const float* ps = part + s2 * (HD + 2);
-      const float c = exp2f(__ldcg(ps) - M);
-      L += __ldcg(ps + 1) * c;
-      A += __ldcg(ps + 2 + dim) * c;
-    }
-    p.o[((int64_t)seq * H + h) * HD + dim] = __float2bfloat16_rn(A / L);
+  // every producer of the grid has fetched past the end before its CTA counts
+  // itself done: the last CTA re-arms the work counters for the next launch
+  if (threadIdx.x == 0 && atomicAdd(p.work + 1, 1) == (int)gridDim.x - 1) {
+    p.work[0] = 0;
+    p.work[1] = 0;
   }
-  if (threadIdx.x == 0) p.counters[seq * p.Hkv + kh] = 0;
+}
+
+bool make_kv_map(CUtensorMap* map, const bf16* pool, int64_t C, int Hkv, int hd, int n_layers) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (hd < 64 || hd % 64) return false;
+  const int64_t rows = C * 2 * Hkv * kBlock;
+  cuuint64_t dims[3] = {(cuuint64_t)hd, (cuuint64_t)rows, (cuuint64_t)std::max(n_layers, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)hd * 2, (cuuint64_t)(rows * hd * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)kBlock, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<bf16*>(pool), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int HD, int G>
-static void launch_v2(const DecodeAttnParams& p, cudaStream_t st) {
-  constexpr int RW = 2;
-  constexpr int R = 4 * RW;
-  constexpr int smem = R * 2 * kBlock * HD * 2 + R * 16 + 4 * G * 2 * 4 + 4 * G * HD * 4 + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_attn_v2_kernel<HD, G, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+static void launch_tc(const DecodeAttnParams& p, cudaStream_t st) {
+  auto kern = decode_attn_tc_kernel<HD, G>;
+  const int smem = TcLayout<HD, G>::bytes(p.n);
+  static int attr = 0;
+  static int occ_smem = -1, occ = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
   }
-  launch_k(decode_attn_v2_kernel<HD, G, RW>, dim3(p.max_splits, p.Hkv, p.n), dim3(160), smem, st, p);
+  if (smem != occ_smem) {   // persistent grid = the CTAs that are resident at once
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTcThreads, smem);
+    occ_smem = smem;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(p.n_items, (int64_t)sms * std::max(occ, 1));
+  launch_k(kern, dim3(grid), dim3(kTcThreads), smem, st, *p.kvmap, p);
 }
 
-static bool v2_enabled() {   // TDPIPE_ATTN_V2=1: smem page-ring kernel (measured slower; A/B only)
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("TDPIPE_ATTN_V2");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
+static bool use_tc(const DecodeAttnParams& p) {
+  const int G = p.H / p.Hkv;
+  if (!p.kvmap || G > 8 || (p.hd != 64 && p.hd != 128) || p.impl == 1) return false;
+  return G >= 2 || p.impl == 2;
 }
 
 template <int HD>
 static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
   const int G = p.H / p.Hkv;
-  if (v2_enabled() && !p.qkv_ws) {
-    switch (G) {
-      case 1: launch_v2<HD, 1>(p, st); return;
-      case 2: launch_v2<HD, 2>(p, st); return;
-      case 4: launch_v2<HD, 4>(p, st); return;
-      case 8: launch_v2<HD, 8>(p, st); return;
-      default: return;
+  if constexpr (HD >= 64) {
+    if (use_tc(p)) {
+      switch (G) {
+        case 1: launch_tc<HD, 1>(p, st); return;
+        case 2: launch_tc<HD, 2>(p, st); return;
+        case 4: launch_tc<HD, 4>(p, st); return;
+        case 8: launch_tc<HD, 8>(p, st); return;
+        default: break;
+      }
     }
   }
   dim3 grid(p.max_splits, p.Hkv, p.n);
@@ -617,54 +1035,70 @@ static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
     case 8: launch_k(decode_attn_kernel<HD, 8>, grid, dim3(128), 0, st, p); break;
     default: return;
   }
-
 }
 
 void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
-  // split size: the largest of 512/256/128 context tokens that still yields
-  // >= 8 CTAs per SM over the batch's actual context lengths (short CTAs of
-  // similar size balance the wave tail; >= 128 tokens amortise a CTA); the
-  // page-ring kernel keeps 6 pages in flight per CTA, so it wants fewer,
-  // longer CTAs: one resident wave of ~4 per SM
-  const bool v2 = v2_enabled();
-  // A/B knobs: CTA target per SM, largest split (tokens, power of two >= 128)
-  static const int tgt_env = std::getenv("TDPIPE_ATTN_TARGET") ? std::atoi(std::getenv("TDPIPE_ATTN_TARGET")) : 0;
-  static const int max_env = std::getenv("TDPIPE_ATTN_MAXSPLIT") ? std::atoi(std::getenv("TDPIPE_ATTN_MAXSPLIT")) : 0;
-  const int64_t target = (int64_t)(tgt_env > 0 ? tgt_env : (v2 ? 4 : 8)) * 148;
-  int split = max_env >= kAttnMinSplit ? max_env : 512, max_ctx = 1;
+  int max_ctx = 1;
   for (int i = 0; i < p.n; ++i) max_ctx = std::max(max_ctx, ctx[i]);
-  for (;;) {
-    int64_t ctas = 0;
-    for (int i = 0; i < p.n; ++i) ctas += (ctx[i] + split - 1) / split;
-    if (ctas * p.Hkv >= target || split <= (v2 ? 256 : kAttnMinSplit)) break;
-    split >>= 1;
-  }
-  // Small batches: the grid is only Hkv x n x splits CTAs (GQA: few kv
-  // heads).  While that is below one CTA per SM, halve the
-  // split (down to 32 tokens) as long as a sequence keeps <= 8 splits (one
-  // merge round trip) and the workspace holds the partials.  Measured on
-  // Llama-2-70B heads (profiles/r1/attn_sweep_gqa8_small.txt): 1.6x at
-  // n <= 4 x 256 tokens (MHA, Llama-2-7B heads: 1.1-1.3x at n <= 2 x 256);
-  // more splits than 8, or splitting a grid that already has >= 1 CTA per
-  // SM, was slower.
-  const int G = p.H / p.Hkv;
-  if (!v2 && split == kAttnMinSplit) {
-    for (;;) {
-      int64_t ctas = 0;
-      for (int i = 0; i < p.n; ++i) ctas += (ctx[i] + split - 1) / split;
-      const int nsplit = split / 2;
-      const int64_t nsplits = (max_ctx + nsplit - 1) / nsplit;
-      if (ctas * p.Hkv >= 148 || nsplit < kAttnMinSplitGQA || nsplits > 8) break;
-      if ((int64_t)p.n * nsplits > p.part_cap) break;
-      split = nsplit;
+  auto ctas_at = [&](int split) {
+    int64_t c = 0;
+    for (int i = 0; i < p.n; ++i) c += (ctx[i] + split - 1) / split;
+    return c * p.Hkv;
+  };
+  int split = 512;
+  if (use_tc(p)) {
+    // persistent tensor-core kernel (2 CTAs per SM): the largest split of
+    // 1024 .. 32 tokens that still gives >= 148 work items (one per SM; the
+    // 2-per-SM grid then balances the rest dynamically), while the partials
+    // fit the workspace and the merge weights (<= kTcMaxSplits splits per
+    // sequence).  Longer splits amortise the per-item q load and merge
+    // (profiles/r2/attn_sweep_gqa8_tc.txt).
+    split = 1024;
+    while ((max_ctx + split - 1) / split > kTcMaxSplits) split *= 2;
+    while (split > kAttnMinSplitGQA && ctas_at(split) < 148) {
+      const int ns = split / 2;
+      if ((int64_t)p.n * ((max_ctx + ns - 1) / ns) > p.part_cap || (max_ctx + ns - 1) / ns > kTcMaxSplits) break;
+      split = ns;
+    }
+  } else {
+    // SIMT kernel: the largest of 512/256/128 context tokens that still
+    // yields >= 8 CTAs per SM over the batch's actual context lengths (short
+    // CTAs of similar size balance the wave tail; >= 128 tokens amortise a
+    // CTA)
+    while (split > kAttnMinSplit && ctas_at(split) < 8 * 148) split >>= 1;
+    // Small batches: the grid is only Hkv x n x splits CTAs (GQA: few kv
+    // heads).  While that is below one CTA per SM, halve the split (down to
+    // 32 tokens) as long as a sequence keeps <= 8 splits (one merge round
+    // trip) and the workspace holds the partials.  Measured on Llama-2-70B
+    // heads (profiles/r1/attn_sweep_gqa8_small.txt): 1.6x at n <= 4 x 256
+    // tokens (MHA, Llama-2-7B heads: 1.1-1.3x at n <= 2 x 256); more splits
+    // than 8, or splitting a grid that already has >= 1 CTA per SM, was slower.
+    if (split == kAttnMinSplit) {
+      for (;;) {
+        const int ns = split / 2;
+        const int64_t nsplits = (max_ctx + ns - 1) / ns;
+        if (ctas_at(split) >= 148 || ns < kAttnMinSplitGQA || nsplits > 8) break;
+        if ((int64_t)p.n * nsplits > p.part_cap) break;
+        split = ns;
+      }
     }
   }
   p.split_tokens = split;
   p.max_splits = (max_ctx + split - 1) / split;
+  p.n_items = ctas_at(split);
 }
 
+// Decode attention is never a PDL dependent: the SIMT kernel issues its first
+// K / V loads before griddepcontrol.wait, which is only safe because the
+// launch waits for its predecessor in the ordinary way; the
+// suppression is enforced here, not left to the caller.
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {
   if (p.n <= 0) return;
+  struct NoPdl {
+    bool prev;
+    NoPdl() : prev(!pdl_enabled()) { pdl_suppress(true); }
+    ~NoPdl() { pdl_suppress(prev); }
+  } no_pdl;
   switch (p.hd) {
     case 16: launch_decode_hd<16>(p, st); break;
     case 32: launch_decode_hd<32>(p, st); break;

@@ -94,6 +94,10 @@ TDP_DEV void pdl_trigger_tail(uint32_t per_sm) {
 bool pdl_enabled();
 // launches from this host thread go without the PDL attribute while on
 void pdl_suppress(bool on);
+// First kernel-launch failure on this host thread since the last take
+// (cudaLaunchKernelEx's return code; the engine checks it per micro-batch).
+void note_launch_error(cudaError_t e);
+cudaError_t take_launch_error();
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
@@ -107,7 +111,7 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  note_launch_error(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 // launch_k with a thread-block cluster of (1, cy, 1)
@@ -128,7 +132,7 @@ inline void launch_kc(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  note_launch_error(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 }  // namespace tdp

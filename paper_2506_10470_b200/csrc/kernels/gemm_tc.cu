@@ -76,27 +76,6 @@ TDP_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar
       : "memory");
 }
 TDP_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-TDP_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-TDP_DEV uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-TDP_DEV void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-TDP_DEV void umma_commit_mc(uint64_t* b, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   smem_u32(b)),
-               "h"(mask)
-               : "memory");
-}
 TDP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 TDP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 TDP_DEV void umma_commit(uint64_t* b) {
@@ -132,11 +111,7 @@ TDP_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// CM > 1: a cluster of CM CTAs along the weight-row dimension shares one
-// token tile; each CTA TMA-loads BN/CM token rows and multicasts them to the
-// whole cluster (cuts L2->SM traffic for the compute-bound prefill GEMMs);
-// every CTA's MMA completion frees the stage in all CTAs (multicast commit).
-template <int BN, int STAGES, int CM>
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, BN <= 128 ? 2 : 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Nf, int T,
                int kb_per_split, int kb_total, EpiParams ep, float* __restrict__ ws, const bf16* __restrict__ wpk,
@@ -165,7 +140,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CM);
+      mbar_init(&empty[s], 1);
     }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -178,13 +153,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  if constexpr (CM > 1) cluster_sync_all();   // peers' barriers exist before any multicast
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t crank = CM > 1 ? cluster_ctarank() : 0;
-  constexpr uint16_t kMask = (uint16_t)((1u << CM) - 1);
-  constexpr int XS = BN / CM;                 // token rows this CTA loads (and multicasts)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -204,10 +175,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         load_w(sa, kb0 + i, &full[i]);
       }
       pdl_wait();
-      auto load_x = [&](uint8_t* dst, int kb, uint64_t* bar) {
-        if constexpr (CM == 1) tma_load_2d(dst, &tmX, kb * BK, n0, bar);
-        else tma_load_2d_mc(dst + crank * XS * 128, &tmX, kb * BK, n0 + (int)crank * XS, bar, kMask);
-      };
+      auto load_x = [&](uint8_t* dst, int kb, uint64_t* bar) { tma_load_2d(dst, &tmX, kb * BK, n0, bar); };
       for (int i = 0; i < pre; ++i) load_x(smem + i * STAGE_BYTES + A_BYTES, kb0 + i, &full[i]);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
@@ -236,8 +204,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)   // advance 16 elements = 32 B inside the swizzle atom
           umma_f16(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
-        if constexpr (CM > 1) umma_commit_mc(&empty[s], kMask);
-        else umma_commit(&empty[s]);
+        umma_commit(&empty[s]);
       }
       umma_commit(accf);
     }
@@ -265,8 +232,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     }
     tc_fence_before();
   }
-  if constexpr (CM > 1) cluster_sync_all();   // no CTA leaves while peers may still signal it
-  else __syncthreads();
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
@@ -274,134 +240,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 }
 
 // ----------------------------------------------------------------------------
-// Token-major tcgen05 GEMM for prefill micro-batches:
+// Token-major tcgen05 GEMM for prefill micro-batches (persistent):
 //   MMA M = 128 tokens (A = activation tile via TMA, 128B swizzle), N = 256
 //   output features (B = two tile-packed 16 KB weight tiles via bulk copies),
 //   K = 64 per stage.  TMEM lane = token, column = feature, so the epilogue
 //   thread of a token holds 32 consecutive features per tcgen05.ld and writes
-//   16-byte vectors (epilogue_row).  Grid: x = token tile (fastest: the token
-//   tiles of one weight tile run together and share it through L2), y = 256-
-//   feature tile.
-template <int STAGES>
-__global__ void __launch_bounds__(192, 1)
-gemm_tn_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int kb_total,
-               EpiParams ep) {
-  constexpr int BNF = 256;
-  constexpr int X_BYTES = 128 * BK * 2;          // 16 KB
-  constexpr int W_BYTES = BNF * BK * 2;          // 32 KB
-  constexpr int STAGE_BYTES = X_BYTES + W_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-
-  pdl_trigger_tail(1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * 128;              // tokens
-  const int n0 = blockIdx.y * BNF;              // features
-  const int wt0 = n0 >> 7;                      // first 128-row packed weight tile
-  const int n_wt = min(2, ((Nf + 127) >> 7) - wt0);   // 1 if the last tile is a half tile
-  const uint32_t stage_tx = X_BYTES + n_wt * (W_BYTES / 2);
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(accf, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(BNF)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      auto load_w = [&](uint8_t* dst, int kb, uint64_t* bar) {
-        for (int h = 0; h < n_wt; ++h)
-          bulk_load(dst + h * (W_BYTES / 2), wpk + (((int64_t)(wt0 + h) * kb_total + kb) << 13), W_BYTES / 2, bar, pol);
-      };
-      const int pre = min(kb_total, STAGES);
-      for (int i = 0; i < pre; ++i) {            // weights first (independent of the previous kernel)
-        mbar_expect_tx(&full[i], stage_tx);
-        load_w(smem + i * STAGE_BYTES + X_BYTES, i, &full[i]);
-      }
-      pdl_wait();
-      for (int i = 0; i < pre; ++i) tma_load_2d(smem + i * STAGE_BYTES, &tmX, i * BK, m0, &full[i]);
-      for (int i = pre; i < kb_total; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], stage_tx);
-        load_w(sa + X_BYTES, i, &full[s]);
-        tma_load_2d(sa, &tmX, i * BK, m0, &full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    pdl_wait();
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BNF >> 3) << 17) |
-                             ((uint32_t)(128 >> 4) << 24);
-      for (int i = 0; i < kb_total; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        const uint64_t ad = smem_desc_sw128(sa);
-        const uint64_t bd = smem_desc_sw128(sa + X_BYTES);
-#pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_f16(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0);
-        umma_commit(&empty[s]);
-      }
-      umma_commit(accf);
-    }
-  } else {
-    pdl_wait();
-    mbar_wait(accf, 0);
-    tc_fence_after();
-    const int q = warp & 3;
-    const int t = m0 + q * 32 + lane;           // this thread's token
-    const bool tok = t < T;
-    int pos = 0, slot = 0;
-    if (tok && ep.mode == kEpiQKV) {
-      pos = ep.pos[t];
-      slot = ep.slot[t];
-    }
-#pragma unroll 1
-    for (int c = 0; c < BNF; c += 32) {
-      if (n0 + c >= Nf) break;
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
-      float v[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      if (tok) epilogue_row(ep, Nf, t, n0 + c, v, pos, slot);
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BNF) : "memory");
-  }
-}
-
-// Persistent variant of gemm_tn_kernel: one CTA per SM walks the (token tile,
+//   16-byte vectors (epilogue_row).  One CTA per SM walks the (token tile,
 // feature tile) grid (token tile fastest, so concurrently running CTAs share a
 // weight tile through L2); the two 256-column TMEM accumulators are double
 // buffered so the epilogue of tile i overlaps the MMAs of tile i+1, and the
@@ -409,7 +253,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__
 template <int STAGES>
 __global__ void __launch_bounds__(192, 1)
 gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int kb_total,
-                EpiParams ep) {
+                EpiParams ep, int nsplit, int kps, float* __restrict__ ws) {
   constexpr int BNF = 256;
   constexpr int X_BYTES = 128 * BK * 2;
   constexpr int W_BYTES = BNF * BK * 2;
@@ -426,7 +270,9 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int MT = (T + 127) / 128;
   const int NT = (Nf + BNF - 1) / BNF;
-  const int n_tiles = MT * NT;
+  // work units: (token tile fastest, feature tile, K split); a split writes
+  // its fp32 partial tile to ws [split][T][Nf] for a split-order reduction
+  const int n_tiles = MT * NT * nsplit;
   const int wtiles = (Nf + 127) >> 7;
 
   if (warp == 0 && lane == 0) {
@@ -459,11 +305,11 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
       int it = 0;   // global k-block counter (ring position)
       bool waited = false;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int m0 = (tile % MT) * 128, nt = tile / MT;
+        const int m0 = (tile % MT) * 128, nt = (tile / MT) % NT, ks = tile / (MT * NT);
         const int wt0 = nt * 2;
         const int n_wt = min(2, wtiles - wt0);
         const uint32_t stage_tx = X_BYTES + n_wt * (W_BYTES / 2);
-        for (int kb = 0; kb < kb_total; ++kb, ++it) {
+        for (int kb = ks * kps; kb < min(kb_total, (ks + 1) * kps); ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
           if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1u);
@@ -492,7 +338,8 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
         if (i >= 2) mbar_wait(&tempty[a], aph ^ 1u);
         tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(a * BNF);
-        for (int kb = 0; kb < kb_total; ++kb, ++it) {
+        const int ks = tile / (MT * NT), kb0 = ks * kps;
+        for (int kb = kb0; kb < min(kb_total, kb0 + kps); ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
           mbar_wait(&full[s], ph);
@@ -502,7 +349,7 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
           const uint64_t bd = smem_desc_sw128(sa + X_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_f16(acc, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+            umma_f16(acc, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           umma_commit(&empty[s]);
         }
         umma_commit(&tfull[a]);
@@ -514,13 +361,13 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
     int i = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
       const int a = i & 1;
-      const int m0 = (tile % MT) * 128, n0 = (tile / MT) * BNF;
+      const int m0 = (tile % MT) * 128, n0 = ((tile / MT) % NT) * BNF, ks = tile / (MT * NT);
       mbar_wait(&tfull[a], (uint32_t)(i >> 1) & 1u);
       tc_fence_after();
       const int t = m0 + q * 32 + lane;
       const bool tok = t < T;
       int pos = 0, slot = 0;
-      if (tok && ep.mode == kEpiQKV) {
+      if (tok && ep.mode == kEpiQKV && !ws) {
         pos = ep.pos[t];
         slot = ep.slot[t];
       }
@@ -532,7 +379,19 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (tok) epilogue_row(ep, Nf, t, n0 + c, v, pos, slot);
+        if (!tok) continue;
+        if (ws) {   // split partial (L2-resident until the split-order reduction reads it)
+          float* wp = ws + ((int64_t)ks * T + t) * Nf + n0 + c;
+          if (n0 + c + 32 <= Nf) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) __stcg(reinterpret_cast<float4*>(wp + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+          } else {
+            for (int j = 0; j < 32; ++j)
+              if (n0 + c + j < Nf) __stcg(wp + j, v[j]);
+          }
+        } else {
+          epilogue_row(ep, Nf, t, n0 + c, v, pos, slot);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -544,242 +403,6 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BNF) : "memory");
   }
-}
-
-// ----------------------------------------------------------------------------
-// Stream-K decode GEMM (swap-AB, T <= BN <= 128 tokens, one token tile).
-// The U = (Nf/128) x (K/64) k-blocks of the weight matrix, in (row tile,
-// k-block) order, are cut into P = min(148, U) contiguous ranges of equal size,
-// one persistent CTA per SM: every SM streams the same number of weight bytes,
-// with no wave tail and no per-tile ramp (the TMA ring runs continuously
-// across tiles; two TMEM accumulators let the epilogue of one segment overlap
-// the MMAs of the next).  A row tile cut by range boundaries has 2+
-// contributors; each writes its fp32 partial [BN][128] to ws and takes a
-// ticket, and the last to arrive sums all partials in contributor order
-// (deterministic) and applies the fused epilogue.  Nothing ever waits on
-// another CTA, so the kernel cannot deadlock whatever the residency.  The
-// owner of a cut tile (the CTA holding its k-block 0) reaches it last in its
-// range, so it usually finds every other partial in place and skips writing
-// its own.
-TDP_DEV int sk_lo(int c, int U, int P) { return (int)(((int64_t)c * U) / P); }
-TDP_DEV int sk_cta_of(int u, int U, int P) {   // the CTA whose range holds k-block u
-  int c = (int)(((int64_t)u * P) / U);
-  while (c + 1 < P && sk_lo(c + 1, U, P) <= u) ++c;
-  while (c > 0 && sk_lo(c, U, P) > u) --c;
-  return c;
-}
-TDP_DEV int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
-gemm_sk_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int KB,
-               EpiParams ep, float* __restrict__ ws, int* __restrict__ tickets) {
-  constexpr int B_BYTES = BN * BK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = 2 * (BN < 32 ? 32 : BN);
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ int s_last[2];
-
-  pdl_trigger();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int MT = (Nf + 127) >> 7;
-  const int U = MT * KB, P = gridDim.x, c = blockIdx.x;
-  const int lo = sk_lo(c, U, P), hi = sk_lo(c + 1, U, P);
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // weights do not depend on the previous kernel: the first stages stream
-      // before the PDL wait, the activation tiles after it
-      const uint64_t pol = policy_evict_first();
-      const int n = hi - lo;
-      const int pre = min(n, STAGES);
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(&full[i], STAGE_BYTES);
-        bulk_load(smem + i * STAGE_BYTES, wpk + ((int64_t)(lo + i) << 13), A_BYTES, &full[i], pol);
-      }
-      pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_2d(smem + i * STAGE_BYTES + A_BYTES, &tmX, ((lo + i) % KB) * BK, 0, &full[i]);
-      for (int i = pre; i < n; ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
-        // packed weights: k-block u of the flattened (row tile, k-block) order
-        // is the u-th 16 KB tile
-        bulk_load(sa, wpk + ((int64_t)(lo + i) << 13), A_BYTES, &full[s], pol);
-        tma_load_2d(sa + A_BYTES, &tmX, ((lo + i) % KB) * BK, 0, &full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    pdl_wait();
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(128 >> 4) << 24);
-      int i = 0, seg = 0;
-      for (int u = lo; u < hi; ++seg) {
-        const int mt = u / KB;
-        const int end = min(hi, (mt + 1) * KB);
-        const int a = seg & 1;
-        if (seg >= 2) mbar_wait(&tempty[a], ((uint32_t)(seg >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t acc = tmem + (uint32_t)(a * BN);
-        for (int u0 = u; u < end; ++u, ++i) {
-          const int s = i % STAGES;
-          mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
-          tc_fence_after();
-          uint8_t* sa = smem + s * STAGE_BYTES;
-          const uint64_t ad = smem_desc_sw128(sa);
-          const uint64_t bd = smem_desc_sw128(sa + A_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_f16(acc, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (u != u0 || k != 0) ? 1u : 0u);
-          umma_commit(&empty[s]);
-        }
-        umma_commit(&tfull[a]);
-      }
-    }
-  } else {
-    pdl_wait();
-    const int q = warp & 3;
-    const int et = threadIdx.x - 64;            // 0..127 over the epilogue warps
-    const int nch = (T + 31) >> 5;
-    int seg = 0;
-    for (int u = lo; u < hi; ++seg) {
-      const int mt = u / KB;
-      const int kb_a = u - mt * KB;
-      const int end = min(hi, (mt + 1) * KB);
-      u = end;
-      const int a = seg & 1;
-      mbar_wait(&tfull[a], (uint32_t)(seg >> 1) & 1u);
-      tc_fence_after();
-      const uint32_t tacc = tmem + (uint32_t)(a * BN) + ((uint32_t)(q * 32) << 16);
-      const int f = mt * 128 + q * 32 + lane;
-      const bool whole = kb_a == 0 && end - mt * KB == KB;
-      if (whole) {
-#pragma unroll 1
-        for (int ch = 0; ch < nch; ++ch) {
-          uint32_t r[32];
-          tmem_ld32(tacc + (uint32_t)(ch * 32), r);
-          epilogue_chunk(ep, T, Nf, f, ch * 32, r);
-        }
-      } else {
-        const int c0 = sk_cta_of(mt * KB, U, P), c1 = sk_cta_of(mt * KB + KB - 1, U, P);
-        const int n = c1 - c0 + 1;
-        const bool owner = c == c0;
-        // partial slots: 2c = a non-owner's (its first segment), 2c+1 = the owner's
-        const int my_slot = owner ? 2 * c + 1 : 2 * c;
-        auto write_partial = [&]() {
-          float* wp = ws + ((int64_t)my_slot * BN) * 128 + q * 32 + lane;
-#pragma unroll 1
-          for (int ch = 0; ch < nch; ++ch) {
-            uint32_t r[32];
-            tmem_ld32(tacc + (uint32_t)(ch * 32), r);
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (ch * 32 + j < T) __stcg(wp + (ch * 32 + j) * 128, __uint_as_float(r[j]));
-          }
-        };
-        int last = 0;
-        if (owner) {
-          if (et == 0) s_last[a] = ld_acquire(tickets + mt) == n - 1;
-          named_bar_sync(1, 128);
-          last = s_last[a];
-          named_bar_sync(1, 128);
-        }
-        if (!last) {
-          write_partial();
-          __threadfence();
-          named_bar_sync(1, 128);
-          if (et == 0) s_last[a] = atomicAdd(tickets + mt, 1) == n - 1;
-          named_bar_sync(1, 128);
-          last = s_last[a];
-        }
-        if (last) {
-          __threadfence();
-          if (et == 0) tickets[mt] = 0;
-#pragma unroll 1
-          for (int ch = 0; ch < nch; ++ch) {
-            uint32_t r[32];
-            tmem_ld32(tacc + (uint32_t)(ch * 32), r);
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            for (int cc = c0; cc <= c1; ++cc) {   // contributor order: deterministic sum
-              if (cc == c) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
-              } else {
-                const float* rp = ws + ((int64_t)(cc == c0 ? 2 * cc + 1 : 2 * cc) * BN + ch * 32) * 128 + q * 32 + lane;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] += ch * 32 + j < T ? __ldcg(rp + j * 128) : 0.f;
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
-            epilogue_chunk(ep, T, Nf, f, ch * 32, r);
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
-  }
-}
-
-template <int BN, int STAGES>
-void launch_sk(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, float* ws, int* tickets,
-               cudaStream_t st) {
-  auto kern = gemm_sk_kernel<BN, STAGES>;
-  constexpr int sm = STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    attr = true;
-  }
-  const int KB = W.K / BK;
-  const int U = ((W.rows + 127) / 128) * KB;
-  launch_k(kern, dim3(std::min(U, kSkCtas)), dim3(192), sm, st, X.map, W.base, W.rows, T, KB, ep, ws, tickets);
 }
 
 // split-K reduction: sums the partials in split order (deterministic) and
@@ -806,10 +429,10 @@ constexpr int smem_bytes() {
   return STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;   // + alignment + barriers
 }
 
-template <int BN, int STAGES, int CM = 1>
+template <int BN, int STAGES>
 void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& ep, int splits, float* ws,
                int* counters, bool defer, cudaStream_t st) {
-  auto kern = gemm_tc_kernel<BN, STAGES, CM>;
+  auto kern = gemm_tc_kernel<BN, STAGES>;
   static bool attr = false;
   constexpr int sm = smem_bytes<BN, STAGES>();
   if (!attr) {
@@ -820,12 +443,8 @@ void launch_bn(const TcOperand& W, const TcOperand& X, int T, const EpiParams& e
   const int kps = (kb_total + splits - 1) / splits;
   const int nsplit = (kb_total + kps - 1) / kps;
   dim3 grid((T + BN - 1) / BN, (W.rows + 127) / 128, nsplit);
-  if constexpr (CM > 1)
-    launch_kc(kern, grid, dim3(192), sm, st, CM, W.map, X.map, W.rows, T, kps, kb_total, ep,
-              nsplit > 1 ? ws : nullptr, W.packed ? W.base : nullptr, counters);
-  else
-    launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
-             W.packed ? W.base : nullptr, counters);
+  launch_k(kern, grid, dim3(192), sm, st, W.map, X.map, W.rows, T, kps, kb_total, ep, nsplit > 1 ? ws : nullptr,
+           W.packed ? W.base : nullptr, counters);
   if (nsplit > 1 && !defer) {
     const int64_t pairs = (int64_t)T * (W.rows / 2);
     const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
@@ -883,117 +502,43 @@ int tc_bn_for(int T, bool decode) {
   return 256;
 }
 
-// TDPIPE_MC=1 enables the cluster-multicast prefill path.  Off by default: the
-// measured sweep (profiles/r1) shows the single-CTA path at 94-106% of the
-// sustained bf16 peak and the multicast variant 5-15% slower.
-static bool mc_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("TDPIPE_MC");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
-}
-
 int effective_splits(int K, int splits) {
   const int kb_total = K / BK;
   const int kps = (kb_total + splits - 1) / splits;
   return (kb_total + kps - 1) / kps;
 }
 
-static bool tnp_enabled() {   // TDPIPE_TNP=0: non-persistent token-major kernel (A/B)
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("TDPIPE_TNP");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
-
-static bool tn_enabled() {   // TDPIPE_TN=0: prefill through the swap-AB kernel (A/B measurements)
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("TDPIPE_TN");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
-
-// TDPIPE_SKGEMM=1 routes decode GEMMs (T <= 128) through the stream-K kernel.
-// Off by default: the isolated sweep (profiles/r1/gemm_sk_sweep.txt) measures
-// it 2-3 us slower per call than the split-K grid at every decode shape (the
-// owner's fix-up of a cut tile adds a dependent L2 round trip at the end of
-// the range, and a full-SM persistent grid leaves no room for the next
-// kernel's PDL prologue).
-static bool sk_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("TDPIPE_SKGEMM");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
-}
-
-bool gemm_sk_applies(const TcOperand& W, int T, bool decode) {
-  return decode && W.packed && T <= 128 && sk_enabled();
-}
-
-int launch_gemm_sk(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, float* ws, int* tickets,
-                   cudaStream_t st) {
-  if (T <= 0) return 1;
-  switch (tc_bn_for(T, true)) {
-    // one CTA per SM with <= 110 KB of smem, so that the next kernel's CTAs
-    // can start (PDL) and prefetch beside it
-    case 32: launch_sk<32, 5>(W, Xby_bn[0], T, ep, ws, tickets, st); break;
-    case 64: launch_sk<64, 4>(W, Xby_bn[1], T, ep, ws, tickets, st); break;
-    default: launch_sk<128, 3>(W, Xby_bn[2], T, ep, ws, tickets, st); break;
-  }
-  return 1;
-}
-
 int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
                    int* counters, bool decode, cudaStream_t st, bool defer_reduce) {
   if (T <= 0) return 1;
-  if (!decode && W.packed && tn_enabled() && T > 128) {
-    // prefill: token-major tiles (vectorised epilogue)
+  if (!decode && W.packed && T > 128) {
+    // prefill: token-major tiles (vectorised epilogue), persistent
     constexpr int STAGES = 4;
     constexpr int sm = STAGES * (128 * BK * 2 + 256 * BK * 2) + 1024 + 256;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(gemm_tn_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      cudaFuncSetAttribute(gemm_tnp_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       attr = true;
     }
-    if (tnp_enabled()) {
-      static bool attr2 = false;
-      if (!attr2) {
-        cudaFuncSetAttribute(gemm_tnp_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        attr2 = true;
-      }
-      const int tiles = ((T + 127) / 128) * ((W.rows + 255) / 256);
-      launch_k(gemm_tnp_kernel<STAGES>, dim3(std::min(tiles, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows,
-               T, W.K / BK, ep);
-      return 1;
+    const int kb_total = W.K / BK;
+    const int kps = (kb_total + std::max(splits, 1) - 1) / std::max(splits, 1);
+    const int nsplit = (kb_total + kps - 1) / kps;
+    const int units = ((T + 127) / 128) * ((W.rows + 255) / 256) * nsplit;
+    launch_k(gemm_tnp_kernel<STAGES>, dim3(std::min(units, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T,
+             kb_total, ep, nsplit, kps, nsplit > 1 ? ws : nullptr);
+    if (nsplit > 1 && !defer_reduce) {
+      const int64_t pairs = (int64_t)T * (W.rows / 2);
+      const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
+      launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, ws, nsplit, T, W.rows, ep);
     }
-    dim3 grid((T + 127) / 128, (W.rows + 255) / 256, 1);
-    launch_k(gemm_tn_kernel<STAGES>, grid, dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T, W.K / BK, ep);
-    return 1;
+    return nsplit;
   }
   switch (tc_bn_for(T, decode)) {
     // <= 110 KB of smem for BN <= 128 so that two CTAs share an SM
     case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, defer_reduce, st); break;
     case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, counters, defer_reduce, st); break;
     case 128: launch_bn<128, 3>(W, Xby_bn[2], T, ep, splits, ws, counters, defer_reduce, st); break;
-    default: {
-      // prefill: cluster the weight-row tiles and multicast the 256-token tile
-      const int mt = (W.rows + 127) / 128;
-      if (mc_enabled() && mt % 4 == 0 && splits <= 1)
-        launch_bn<256, 4, 4>(W, Xby_bn[1], T, ep, 1, ws, counters, defer_reduce, st);
-      else if (mc_enabled() && mt % 2 == 0 && splits <= 1)
-        launch_bn<256, 4, 2>(W, Xby_bn[2], T, ep, 1, ws, counters, defer_reduce, st);
-      else
-        launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, defer_reduce, st);
-      break;
-    }
+    default: launch_bn<256, 4>(W, Xby_bn[3], T, ep, splits, ws, counters, defer_reduce, st); break;
   }
   return effective_splits(W.K, splits);
 }

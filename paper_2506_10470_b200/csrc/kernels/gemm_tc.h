@@ -29,15 +29,4 @@ int tc_bn_for(int T, bool decode);
 int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
                    int* counters, bool decode, cudaStream_t st, bool defer_reduce = false);
 
-// Stream-K decode GEMM (T <= 128, packed weights): P = min(148, tiles x
-// k-blocks) persistent CTAs over equal contiguous k-block ranges; cut tiles
-// are combined through ws [2 * kSkCtas][128][128] fp32 by the last arriving
-// contributor (tickets: >= Nf/128 zero-initialised ints, left zeroed).
-// Applies ep directly (no deferred reduction); returns 1.
-constexpr int kSkCtas = 148;
-constexpr int64_t kSkWsFloats = 2LL * kSkCtas * 128 * 128;
-bool gemm_sk_applies(const TcOperand& W, int T, bool decode);
-int launch_gemm_sk(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, float* ws, int* tickets,
-                   cudaStream_t st);
-
 }  // namespace tdp

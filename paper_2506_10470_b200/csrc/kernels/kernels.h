@@ -1,5 +1,6 @@
 // kernels.h -- host-side launchers of the sm_100a kernels (all async on `st`).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -8,6 +9,8 @@ namespace tdp {
 
 // launches from this host thread go without the PDL attribute while on (misc.cu)
 void pdl_suppress(bool on);
+// first kernel-launch failure on this host thread since the last call (misc.cu)
+cudaError_t take_launch_error();
 
 typedef __nv_bfloat16 bf16;
 
@@ -70,7 +73,6 @@ struct EpiParams {
   const float* rope_cs;  // [max_pos][hd/2][2] (cos, sin)
   int H, Hkv, hd;
 };
-void launch_gemm(const bf16* A, const bf16* W, int M, int N, int K, const EpiParams& ep, cudaStream_t st);
 
 // ---- attention --------------------------------------------------------------
 // Decode: one query token per sequence; q [n, H*hd] (physical RoPE-pair order),
@@ -97,7 +99,19 @@ struct DecodeAttnParams {
   int qkv_splits = 0, nqkv = 0;
   const float* rope_cs = nullptr;   // [max_pos][hd/2][2] (cos, sin)
   int64_t part_cap = 0;  // part[] capacity in (sequence x split) slots per head (0: no GQA small splits)
+  // TMA view of the whole KV pool (make_kv_map) and this layer's index in it:
+  // the tensor-core GQA kernel (G > 1, hd 64 / 128) stages K/V pages through
+  // it; nullptr -> the SIMT kernel
+  const CUtensorMap* kvmap = nullptr;
+  int layer = 0;
+  int* work = nullptr;   // [2] zero-initialised work-item / done counters (re-armed by the kernel)
+  int64_t n_items = 0;   // (sequence, split, kv head) items of the plan (plan_decode_attn)
+  int impl = 0;          // 0: kernel by shape (tensor cores for GQA hd 64/128); 1: SIMT; 2: tensor cores (td_bench_attn)
 };
+// 3-D TMA descriptor of a KV pool [n_layers][C blocks][K|V][Hkv][16][hd] bf16
+// viewed as (hd, C*2*Hkv*16 page rows, n_layers), box (64, 16, 1), 128B
+// swizzle: one box = half (hd 128) or all (hd 64) of a 16-token K or V page.
+bool make_kv_map(CUtensorMap* map, const bf16* pool, int64_t C, int Hkv, int hd, int n_layers);
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 // Launch plan from the host copy of the context lengths: sets split_tokens
 // and max_splits (part[] must hold cdiv(max_seq_len, kAttnMinSplit) splits per

@@ -21,13 +21,16 @@ namespace tdp {
 static thread_local int g_pdl_suppress = 0;
 void pdl_suppress(bool on) { g_pdl_suppress = on ? 1 : 0; }
 
-bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("TDPIPE_PDL");
-    on = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
-  }
-  return on == 1 && !g_pdl_suppress;
+bool pdl_enabled() { return !g_pdl_suppress; }
+
+static thread_local cudaError_t g_launch_err = cudaSuccess;
+void note_launch_error(cudaError_t e) {
+  if (e != cudaSuccess && g_launch_err == cudaSuccess) g_launch_err = e;
+}
+cudaError_t take_launch_error() {
+  const cudaError_t e = g_launch_err;
+  g_launch_err = cudaSuccess;
+  return e;
 }
 
 // splitmix64 finaliser (counter-based; both sides implement it independently)
@@ -82,6 +85,7 @@ void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st) {
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 64) blocks = 148 * 64;
   init_kernel<<<blocks, 256, 0, st>>>(dst, s, seed);
+  note_launch_error(cudaGetLastError());
 }
 
 // ----------------------------------------------------------------- embedding
@@ -288,7 +292,7 @@ void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf1
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<8>, ws, splits, x, g, out, T, d, eps, xpeer);
+    note_launch_error(cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<8>, ws, splits, x, g, out, T, d, eps, xpeer));
   } else {
     launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps, xpeer);
   }
@@ -387,6 +391,7 @@ void launch_token_pairs(const int32_t* arena, const int32_t* outpos, int n, int3
 void launch_token_scatter(const int32_t* pairs, int n, int32_t* arena, cudaStream_t st) {
   if (n <= 0) return;
   token_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(pairs, n, arena);
+  note_launch_error(cudaGetLastError());
 }
 
 

@@ -23,8 +23,7 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
   cudaStreamCreate(&s);
   if (cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dW, (size_t)N * K * 2) ||
       cudaMalloc(&dO, (size_t)T * N * 4) ||
-      cudaMalloc(&ws, std::max<size_t>((size_t)std::max(splits, 1) * (Tcap + 256) * ((N + 127) / 128 * 128),
-                                        (size_t)kSkWsFloats) * 4) ||
+      cudaMalloc(&ws, (size_t)std::max(splits, 1) * (Tcap + 256) * ((N + 127) / 128 * 128) * 4) ||
       cudaMalloc(&cnt, 65536 * sizeof(int))) {
     st = TD_ENOMEM;
   } else {
@@ -36,14 +35,14 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
     ep.mode = kEpiF32;
     ep.out_f32 = dO;
     ep.ldo = N;
-    if (impl == 1) {
-      launch_gemm(dA, dW, T, N, K, ep, s);
+    if (impl != 0 && impl != 2 && impl != 4) {
+      st = TD_EINVAL;
     } else {
       // impl 0: tile-packed weights (the engine's layout); impl 2: row-major W via TMA
       TcOperand w, x[4];
       bool ok = true;
       bf16* dP = nullptr;
-      if (impl == 0 || impl == 3) {
+      if (impl == 0 || impl == 4) {
         const int Np = (N + 127) / 128 * 128;
         std::vector<uint16_t> pk((size_t)Np * K, 0);
         for (int r = 0; r < N; ++r)
@@ -56,7 +55,7 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
       }
       for (int i = 0; i < 4; ++i) ok = ok && make_tc_operand(&x[i], dA, Tcap, K, 32 << i);
       if (!ok) st = TD_ECUDA;
-      else if (impl == 3) launch_gemm_sk(w, x, T, ep, ws, cnt, s);
+      else if (impl == 4) launch_gemm_tc(w, x, T, ep, splits, ws, cnt, /*decode=*/false, s);   // token-major (+ split-K)
       else launch_gemm_tc(w, x, T, ep, splits, ws, cnt, splits > 1, s);
       cudaStreamSynchronize(s);
       cudaFree(dP);
@@ -89,7 +88,7 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
   for (auto& w : Ws)
     if (cudaMalloc(&w, (size_t)Np * K * 2) != cudaSuccess) st = TD_ENOMEM;
   if (st || cudaMalloc(&dA, (size_t)Tcap * K * 2) || cudaMalloc(&dO, (size_t)T * N * 4) ||
-      cudaMalloc(&ws, std::max<size_t>((size_t)std::max(splits, 1) * (Tcap + 256) * Np, (size_t)kSkWsFloats) * 4) ||
+      cudaMalloc(&ws, (size_t)std::max(splits, 1) * (Tcap + 256) * Np * 4) ||
       cudaMalloc(&cnt, 65536 * 4)) {
     st = TD_ENOMEM;
   } else {
@@ -109,8 +108,7 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
       st = TD_ECUDA;
     } else {
       auto call = [&](int i) {
-        if (decode == 2) launch_gemm_sk(w[i % copies], x, T, ep, ws, cnt, s);
-        else launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode != 0, s);
+        launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode == 1, s);   // 2: token-major (+ split-K)
       };
       for (int i = 0; i < 3; ++i) call(i);
       cudaEvent_t a, b;
@@ -140,7 +138,8 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
 // pages scattered through the pool the way the block allocator hands them out;
 // iterations rotate over `copies` disjoint page sets so the K/V stream from HBM.
 extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx, int32_t H, int32_t Hkv, int32_t hd,
-                                   int32_t iters, float* us_per_call) {
+                                   int32_t iters, int32_t split, int32_t impl, float* us_per_call) {
+  if (split != 0 && (split < kAttnMinSplitGQA || split % 16)) return TD_EINVAL;
   if (n < 1 || !ctx || H < 1 || Hkv < 1 || H % Hkv || iters < 1 || !us_per_call) return TD_EINVAL;
   if (hd != 16 && hd != 32 && hd != 64 && hd != 128) return TD_EINVAL;
   const int G = H / Hkv;
@@ -181,17 +180,27 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
   if (cudaMalloc(&kv, pool * blk_bytes) || cudaMalloc(&q, (size_t)n * H * hd * 2) ||
       cudaMalloc(&o, (size_t)n * H * hd * 2) || cudaMalloc(&part, (size_t)n * H * cap * (hd + 2) * 4) ||
       cudaMalloc(&dctx, n * 4) || cudaMalloc(&dbt, bt.size() * 4) ||
-      cudaMalloc(&cnt, (size_t)n * Hkv * 4)) {
+      cudaMalloc(&cnt, ((size_t)n * Hkv + 2) * 4)) {
     st = TD_ENOMEM;
   } else {
     cudaMemset(kv, 0, pool * blk_bytes);
     cudaMemset(q, 0, (size_t)n * H * hd * 2);
-    cudaMemset(cnt, 0, (size_t)n * Hkv * 4);
+    cudaMemset(cnt, 0, ((size_t)n * Hkv + 2) * 4);
     cudaMemcpy(dctx, ctx, n * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice);
     DecodeAttnParams p{q, kv, dctx, dbt, maxblk, o, part, 0, n, H, Hkv, hd, 0, cnt};
     p.part_cap = (int64_t)n * cap;
+    p.work = cnt + (size_t)n * Hkv;
+    CUtensorMap kvmap;
+    if (hd >= 64 && make_kv_map(&kvmap, kv, pool, Hkv, hd, 1)) p.kvmap = &kvmap;
+    p.impl = impl;
     plan_decode_attn(p, ctx);
+    if (split) {
+      p.split_tokens = split;
+      p.max_splits = (max_ctx + split - 1) / split;
+      p.n_items = 0;
+      for (int i = 0; i < n; ++i) p.n_items += (int64_t)((ctx[i] + split - 1) / split) * Hkv;
+    }
     auto run = [&](int i) {
       DecodeAttnParams pi = p;
       pi.bt = dbt + (size_t)(i % copies) * n * maxblk;

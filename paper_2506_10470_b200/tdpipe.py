@@ -71,7 +71,7 @@ EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
            "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace",
-           "td_get_weight"]
+           "td_get_weight", "td_bench_step"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_run.argtypes = [C.c_void_p, P(td_run_stats)]
     lib.td_get_output.argtypes = [C.c_void_p, C.c_int64, P(C.c_int32), C.c_int32, P(C.c_int32)]
     lib.td_get_outputs.argtypes = [C.c_void_p, P(C.c_int32), C.c_int32, C.c_int32, P(C.c_int32)]
+    lib.td_bench_step.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
+                                  P(C.c_double)]
     lib.td_get_weight.argtypes = [C.c_void_p, C.c_int32, P(C.c_uint16), C.c_int64, P(C.c_int64), P(C.c_int64)]
     lib.td_get_logits.argtypes = [C.c_void_p, C.c_int64, P(C.c_float), C.c_int64, P(C.c_int32)]
     lib.td_reset.argtypes = [C.c_void_p]
@@ -106,7 +108,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                   P(C.c_double)]
     lib.td_nccl_ids.argtypes = [C.c_void_p]
     lib.td_bench_gemm.argtypes = [C.c_int32] * 8 + [P(C.c_float)]
-    lib.td_bench_attn.argtypes = [C.c_int32, C.c_int32, P(C.c_int32)] + [C.c_int32] * 4 + [P(C.c_float)]
+    lib.td_bench_attn.argtypes = [C.c_int32, C.c_int32, P(C.c_int32)] + [C.c_int32] * 6 + [P(C.c_float)]
     lib.td_simulate.argtypes = [C.c_void_p, P(td_run_stats), C.c_int64]
     lib.td_write_trace.argtypes = [C.c_void_p, C.c_char_p]
     lib.td_test_gemm.argtypes = [C.c_int32, P(C.c_uint16), P(C.c_uint16), C.c_int32, C.c_int32, C.c_int32,
@@ -245,6 +247,14 @@ class TDPipe:
                     "td_get_outputs")
         return out, n
 
+    def td_bench_step(self, kind: int, n_seqs: int, length: int, iters: int = 10):
+        """(mean step us, speed-of-light us) of one synthetic micro-batch; per-kernel
+        timing is then readable with td_get_timing."""
+        us, ideal = C.c_double(), C.c_double()
+        self._check(lib().td_bench_step(self.ctx, int(kind), int(n_seqs), int(length), int(iters), C.byref(us),
+                                        C.byref(ideal)), "td_bench_step")
+        return us.value, ideal.value
+
     def td_get_weight(self, tensor_id: int) -> np.ndarray:
         """bf16 bit patterns (uint16) of F9 tensor `tensor_id`, logical [rows, cols]."""
         r, c = C.c_int64(), C.c_int64()
@@ -349,12 +359,14 @@ def td_bench_gemm(T: int, N: int, K: int, splits: int = 1, decode: bool = True, 
     return us.value
 
 
-def td_bench_attn(ctx, H: int, Hkv: int, hd: int, iters: int = 50, device: int = 0) -> float:
+def td_bench_attn(ctx, H: int, Hkv: int, hd: int, iters: int = 50, device: int = 0, split: int = 0,
+                  impl: int = 0) -> float:
     """Average device microseconds per decode-attention launch over context
-    lengths `ctx` (the engine's launch plan)."""
+    lengths `ctx` (the engine's launch plan, or `split`-token splits)."""
     c = np.ascontiguousarray(ctx, dtype=np.int32)
     us = C.c_float(0)
-    st = lib().td_bench_attn(device, len(c), _ptr(c, C.c_int32), H, Hkv, hd, iters, C.byref(us))
+    st = lib().td_bench_attn(device, len(c), _ptr(c, C.c_int32), H, Hkv, hd, iters, int(split), int(impl),
+                             C.byref(us))
     if st != TD_OK:
         raise TDError(f"td_bench_attn failed: {st}")
     return us.value

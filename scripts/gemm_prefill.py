@@ -11,5 +11,5 @@ for T in [2048, 1024]:
     for name, (N, K) in shapes.items():
         us = td_bench_gemm(T, N, K, 1, False, iters=20, copies=2)
         tf = 2.0 * T * N * K / (us * 1e-6) / 1e12
-        print(json.dumps(dict(T=T, gemm=name, mc=os.environ.get("TDPIPE_MC", "1"), us=round(us, 1), TFLOPs=round(tf, 1),
+        print(json.dumps(dict(T=T, gemm=name, us=round(us, 1), TFLOPs=round(tf, 1),
                               frac_sustained=round(tf / 1406.7, 3))), flush=True)

@@ -25,6 +25,9 @@ def dram_total(path):
 
 
 out, args = sys.argv[1], sys.argv[2:]
+src = None
+if args and args[0].startswith("--source="):
+    src, args = args[0][len("--source="):], args[1:]
 caps, D, A, N = [], 0.0, 0.0, 0
 for c, j in zip(args[::2], args[1::2]):
     dram, n = dram_total(c)
@@ -39,7 +42,6 @@ for c, j in zip(args[::2], args[1::2]):
 res = {"kernel": "decode_attn", "launches": N, "dram_bytes_per_launch": D / N, "algorithmic_bytes_per_launch": A / N,
        "ratio": D / A, "captures": caps,
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none over every "
-                 "decode_attn launch of scripts/traffic_attn.py (engine decode steps, Llama-2-7B, 32 layers, "
-                 "ShareGPT-like contexts, scattered pages)"}
+                 "decode_attn launch of " + (src or "the captured runs") + " (engine path)"}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res))

@@ -68,7 +68,8 @@ def _shape(case):
 
 def _opts(case, csv):
     return dict(kv_blocks=case["kv_blocks"], profile_csv=csv, prefill_token_budget=case["budget"],
-                max_batch_seqs=8, fp_stride=4, fp_horizon=16, record_logits=case["logits"], device=0)
+                max_batch_seqs=case.get("max_seqs", 8), hb_tokens=case.get("hb_tokens", 512), fp_stride=4,
+                fp_horizon=16, record_logits=case["logits"], device=0)
 
 
 def _worker(rank, world, port, csv, case, q):
@@ -120,6 +121,11 @@ CASES = [
     # micro-batches (wraps the 3-slot residual ring and the 16-slot token ring)
     dict(name="starved_pp2", wl="rand", seed=7, layers=2, world=2, kv_blocks=12, budget=64, logits=0),
     dict(name="starved_pp4", wl="rand", seed=11, layers=4, world=4, kv_blocks=12, budget=64, logits=0),
+    # decode groups (n_live / W, + steals) far above max_batch_seqs = 2: the
+    # hand-off slots sized at td_create are too small and td_run re-sizes
+    # every rank's mailbox before the first launch
+    dict(name="big_decode_pp2", wl="rand", seed=9, layers=2, world=2, kv_blocks=400, budget=2048, logits=0,
+         max_seqs=2, hb_tokens=0),
 ]
 
 

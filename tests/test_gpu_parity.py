@@ -492,3 +492,43 @@ def test_gqa_small_batch_32_token_splits():
             _rows_ok(out[i], ref[-2])
             _rows_ok(out2[i], ref[-1])
     t.close()
+
+
+def test_td_run_trace_and_kv_timeline(tmp_path):
+    """A td_run with timing on leaves its CUDA-event spans and the KV-usage
+    timeline (PAPER.md:580-585 fig:memory_usage) for td_write_trace: one span
+    per (micro-batch, stage) in launch order, non-overlapping on the single
+    stream, and the KV blocks held at every launch equal those of td_simulate
+    for the same request set -- both come from the same controller decisions
+    (the allocation the GPU run performed is the one the controller planned)."""
+    import json
+    from paper_2506_10470_b200 import TD_EXEC_NULL
+    shape = SHAPES["tiny_gqa"].with_layers(2)
+    csv = str(tmp_path / "p.csv")
+    write_profile_csv(csv, *synthetic_profile(64, 2048, knee=8))
+    wl = random_tiny_workload(8, n_max=14, len_max=40)
+    C = max((len(r.prompt) + r.max_new_tokens + 15) // 16 for r in wl.requests) + 3
+    opts = dict(kv_blocks=C, profile_csv=csv, prefill_token_budget=64, max_batch_seqs=8, fp_stride=4, fp_horizon=16)
+    t = TDPipe(shape, 2, **opts)
+    t.submit_workload(wl)
+    t.td_set_timing(True)
+    st = t.td_run()
+    path = str(tmp_path / "run.json")
+    t.td_write_trace(path)
+    t.close()
+    ev = json.load(open(path))["traceEvents"]
+    spans = [e for e in ev if e["ph"] == "X"]
+    kv = [e["args"]["blocks"] for e in ev if e["ph"] == "C"]
+    assert len(spans) == 2 * st["n_microbatches"] and len(kv) == st["n_microbatches"]
+    ss = sorted((e["ts"], e["ts"] + e["dur"]) for e in spans)
+    assert all(a[1] <= b[0] + 1e-3 for a, b in zip(ss, ss[1:]))     # one stream: stages back to back
+    assert max(e["ts"] + e["dur"] for e in spans) <= st["makespan_ns"] / 1e3 + 1e-3
+    s = TDPipe(shape, 2, executor=TD_EXEC_NULL, **opts)
+    s.submit_workload(wl)
+    s.td_simulate(0)
+    path2 = str(tmp_path / "sim.json")
+    s.td_write_trace(path2)
+    s.close()
+    kv_sim = [e["args"]["blocks"] for e in json.load(open(path2))["traceEvents"] if e["ph"] == "C"]
+    assert kv == kv_sim
+    assert max(kv) <= C
