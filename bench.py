@@ -457,6 +457,8 @@ def run_ours(args):
         d2h = int(sum(len(r.prompt) + r.max_new_tokens + 1 for r in wl.requests) * 4)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "scope": f"N=1 point of the metric's 1/2/4/8-GPU series: one B200, {args.stages} pipeline stage(s) in one "
+                 f"process (the multi-GPU pipeline runs under torchrun)",
         "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": dict(workload_config(args), kv_blocks=info["kv_blocks"], profile_s=round(prof_s, 2)),

@@ -286,6 +286,14 @@ td_status td_get_timing(struct td_ctx* ctx, const char* name, int64_t* launches,
 td_status td_bench_step(struct td_ctx* ctx, int32_t kind, int32_t n_seqs, int32_t len, int32_t iters,
                         double* step_us, double* ideal_us);
 
+/* Algorithmic bytes of every launch of kernel class `name` accumulated by
+ * per-kernel timing (td_set_timing), in launch order -- lets a DRAM-traffic
+ * capture of a subset of a run's launches (ncu) be compared with exactly the
+ * same launches' algorithmic bytes.  *n = number of launches; copies
+ * min(cap, n) values into `out` (nullable: size query).  TD_ERANGE if cap < n
+ * and out != NULL. */
+td_status td_get_launch_bytes(struct td_ctx* ctx, const char* name, double* out, int64_t cap, int64_t* n);
+
 /* Kernel unit test (testing only): out[T, N] fp32 = A[T, K] . W[N, K]^T with
  * A, W given as bf16 bit patterns (host), on the tcgen05 kernels: impl 0
  * packs W into the tile-packed layout the engine uses, impl 2 reads row-major

@@ -585,6 +585,17 @@ extern "C" td_status td_get_weight(td_ctx* c, int32_t tensor_id, uint16_t* out, 
   return TD_OK;
 }
 
+extern "C" td_status td_get_launch_bytes(td_ctx* c, const char* name, double* out, int64_t cap, int64_t* n) {
+  if (!c || !name || !n) return TD_EINVAL;
+  KernelTiming t;
+  if (!c->engine || !c->engine->get_timing(name, &t)) return TD_EINVAL;
+  *n = (int64_t)t.launch_bytes.size();
+  if (!out) return TD_OK;
+  if (cap < *n) return fail(c, TD_ERANGE, "cap < launches");
+  std::memcpy(out, t.launch_bytes.data(), t.launch_bytes.size() * sizeof(double));
+  return TD_OK;
+}
+
 // NCCL is loaded lazily (dlopen) so that single-process and CPU-only use never
 // needs it; td_nccl_ids returns two ncclUniqueIds (forward and token-return comms).
 typedef int (*nccl_get_unique_id_fn)(void*);

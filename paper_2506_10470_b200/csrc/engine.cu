@@ -577,22 +577,17 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
   int splits = 1;
   if (decode && T > 128) {
     // 129..512-token decode batches are near (or past) the tensor roof: the
-    // token-major kernel (128 tokens x 256 features per tile), with split-K
-    // when the tiles alone fill the 148 SMs badly: the split count (<= 8,
-    // >= 8 k-blocks per split, partials within the L2-sized workspace) that
-    // maximises the persistent grid's occupancy units / (rounds x 148); ties
-    // keep fewer splits
+    // token-major kernel (128 tokens x 256 features per tile).  The residual
+    // GEMMs (O, down: their split partials are summed by the resid_norm launch
+    // that follows anyway) split K when their tiles fill the 148 SMs badly
+    // (< 96 tiles): the fewest splits giving >= 128 units, >= 16 k-blocks
+    // each.  Measured per shape in profiles/r2/gemm_sweep_t128.txt.
     decode = false;
     const int64_t tiles = (int64_t)((T + 127) / 128) * ((N + 255) / 256);
-    double best = 0.0;
-    for (int sp = 1; sp <= 8; ++sp) {
-      if (sp > 1 && ((K / 64) / sp < 8 || (int64_t)sp * T * ((N + 127) / 128 * 128) > ws_cap_)) break;
-      const int64_t units = tiles * sp;
-      const double eff = (double)units / (double)(((units + 147) / 148) * 148);
-      if (eff > best + 0.02) {
-        best = eff;
-        splits = sp;
-      }
+    if (ep.mode == kEpiResid && defer && tiles < 96) {
+      while (splits < 4 && tiles * splits < 128 && (K / 64) / (splits + 1) >= 16 &&
+             (int64_t)(splits + 1) * T * ((N + 127) / 128 * 128) <= ws_cap_)
+        ++splits;
     }
   } else if (decode) {
     // split-K to ~288 CTAs (about 2 per SM), at most 8 splits, >= 4 k-blocks
@@ -685,6 +680,7 @@ double CudaEngine::accumulate_timed() {
       kt.ms += t;
       kt.bytes += tl.bytes;
       kt.flops += tl.flops;
+      if (c == tl.cls) kt.launch_bytes.push_back(tl.bytes);
     }
     if (tl.cls == cStage) busy += t;
   }

@@ -27,6 +27,7 @@ struct KernelTiming {
   double ms = 0.0;
   double bytes = 0.0;
   double flops = 0.0;
+  std::vector<double> launch_bytes;   // algorithmic bytes of every launch, in launch order
 };
 
 // One (micro-batch, stage) span of a timed td_run, ns from the run's first

@@ -156,79 +156,6 @@ __device__ __forceinline__ void attn_finish(const DecodeAttnParams& p, int seq, 
 
 
 
-// Fused QKV split-K epilogue of the tensor-core kernel's q-prep warp (the SIMT
-// kernel inlines the same arithmetic): q of the G heads of kv head kh, plus
-// k / v of the newest token when `has_new`; partials summed in split order,
-// RoPE at position `newest` on the interleaved (i, i+hd/2) pairs, bf16 -- bit
-// for bit the arithmetic of splitk_reduce_kernel.  s_qkv = [q_0 .. q_{G-1},
-// k, v] x HD.
-template <int HD, int G, int NBT>
-TDP_DEV void fused_qkv_reduce(const DecodeAttnParams& p, int seq, int kh, int newest, bool has_new, bf16* s_qkv,
-                              int tid, int nthr) {
-  // NBT pairs per thread per round: all their split partials are loaded
-  // before any is summed (NBT x 8 float2 in flight per thread)
-  const int H = p.H;
-  const int npairs = (G + (has_new ? 2 : 0)) * (HD / 2);
-  for (int p0 = tid; p0 < npairs; p0 += nthr * NBT) {
-    float2 pr[NBT][8];
-    int fs[NBT];
-    bool rp[NBT];
-#pragma unroll
-    for (int u = 0; u < NBT; ++u) {
-      const int e = (p0 + u * nthr) * 2;
-      int f = 0;
-      bool rope = true;
-      if (e < G * HD) f = kh * G * HD + e;
-      else if (e < (G + 1) * HD) f = (H + kh) * HD + (e - G * HD);
-      else { f = (H + p.Hkv + kh) * HD + (e - (G + 1) * HD); rope = false; }
-      fs[u] = f;
-      rp[u] = rope;
-      const bool ok = p0 + u * nthr < npairs;
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2)
-        if (ok && s2 < p.qkv_splits)
-          pr[u][s2] = __ldcg(reinterpret_cast<const float2*>(p.qkv_ws + ((int64_t)s2 * p.n + seq) * p.nqkv + f));
-    }
-#pragma unroll
-    for (int u = 0; u < NBT; ++u) {
-      if (p0 + u * nthr >= npairs) break;
-      const int e = (p0 + u * nthr) * 2, f = fs[u];
-      const float2 cs = rp[u] ? *reinterpret_cast<const float2*>(p.rope_cs + ((int64_t)newest * (HD >> 1) + ((f % HD) >> 1)) * 2)
-                              : make_float2(1.f, 0.f);
-      float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2)
-        if (s2 < p.qkv_splits) { v0 += pr[u][s2].x; v1 += pr[u][s2].y; }
-      for (int s2 = 8; s2 < p.qkv_splits; ++s2) {
-        const float2 q2 = __ldcg(reinterpret_cast<const float2*>(p.qkv_ws + ((int64_t)s2 * p.n + seq) * p.nqkv + f));
-        v0 += q2.x;
-        v1 += q2.y;
-      }
-      float r0 = v0, r1 = v1;
-      if (rp[u]) {
-        r0 = v0 * cs.x - v1 * cs.y;
-        r1 = v1 * cs.x + v0 * cs.y;
-      }
-      *reinterpret_cast<uint32_t*>(s_qkv + e) = pack_bf16x2(r0, r1);
-    }
-  }
-}
-
-// The newest token's K / V (s_qkv[G], s_qkv[G+1]) into its paged-cache slot:
-// threads tid < HD/8 store one 16-byte chunk of each (after a barrier that
-// follows fused_qkv_reduce).
-template <int HD, int G>
-TDP_DEV void store_new_kv(const DecodeAttnParams& p, int seq, int kh, int newest, const bf16* s_qkv, int tid) {
-  if (tid >= HD / 8) return;
-  const int64_t head_stride = (int64_t)kBlock * HD;
-  const int32_t* bt = p.bt + (int64_t)seq * p.maxblk;
-  const int64_t kb = (((int64_t)bt[newest >> 4] * 2) * p.Hkv + kh) * head_stride + (newest & 15) * HD + tid * 8;
-  bf16* kvw = const_cast<bf16*>(p.kv);
-  *reinterpret_cast<uint4*>(kvw + kb) = *reinterpret_cast<const uint4*>(s_qkv + G * HD + tid * 8);
-  *reinterpret_cast<uint4*>(kvw + kb + (int64_t)p.Hkv * head_stride) =
-      *reinterpret_cast<const uint4*>(s_qkv + (G + 1) * HD + tid * 8);
-}
-
 // One CTA attends (sequence seq, kv head kh) over context tokens
 // [t_begin, t_end): segment `split` of `n_splits`.  With n_splits == 1 it writes
 // o; otherwise it writes the segment's partial (m, l, acc) and the last
@@ -455,8 +382,9 @@ decode_attn_kernel(DecodeAttnParams p) {
 //    with 3 shuffles, per-thread partial sums reduced once at the end;
 //  * warps merge through shared memory, then the split merge of the SIMT
 //    kernel (partials in split order, last CTA merges).
-// The newest token of a fused-QKV decode step is not in the cache yet: it is
-// left out of the streamed range and added in the merge (as the SIMT kernel).
+// q comes from the QKV GEMM's epilogue (or its split-K reduce), which has also
+// written the newest token's K / V into the cache: the kernel never runs in the
+// SIMT kernel's fused-QKV mode (launch_decode_attn falls back if asked to).
 namespace {
 TDP_DEV void tc_mbar_init(uint64_t* b, uint32_t c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
@@ -518,7 +446,7 @@ struct TcLayout {
   static constexpr int SLOT = 2 * PAGE;
   static constexpr int RING = kTcRing * SLOT;
   static constexpr int OBUF = 4 * (G * (HD + kTcPad) + 2 * 8) * 4;   // 4 warps: O^T rows, then m[8], l[8]
-  static constexpr int QBUF = (G + 2) * HD * 2;                // q of G heads, newest k, v
+  static constexpr int QBUF = G * HD * 2;                      // q of the G heads
   static constexpr int BARS = (2 * kTcRing + 3 * kTcItemQ + 4) * 8;
   static constexpr int FIXED = RING + 2 * OBUF + kTcItemQ * QBUF + BARS + 1024;   // + alignment
   static int bytes(int n) { return FIXED + (n + 1) * 4; }
@@ -531,13 +459,12 @@ struct TcLayout {
 //             streams each item's K / V pages into the page ring by TMA
 //             (block-table entries read 32 at a time by the whole warp);
 //   q-prep    (warp 5): for each queued item stages q of its G heads in
-//             shared memory (one bulk copy, or the fused QKV split-K reduce +
-//             RoPE, which also writes the newest token's K / V to the cache);
+//             shared memory (one bulk copy);
 //   consumers (warps 0-3): per item, tensor-core S^T / online softmax / O^T
 //             over every 4th page, then their (m, l, O) into one of two
 //             result buffers;
-//   merger    (warp 6): combines the 4 warps (+ the newest token of a fused
-//             step), writes o or the split partial, and the last split of a
+//   merger    (warp 6): combines the 4 warps, writes o or the split
+//             partial, and the last split of a
 //             (sequence, kv head) merges all partials in split order.
 // So q loads, merges and split merges of one item overlap the page streaming
 // of the next.  Local page j of an item always goes to consumer warp j mod 4
@@ -573,14 +500,11 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = p.H;
-  const bool fused = p.qkv_ws != nullptr;
   const float scale = rsqrtf((float)HD) * kLog2e;
   struct Item {
     int seq, kh, split, n_splits, t_begin, t_end, pg0, npg;
-    bool has_new;
   };
   // item idx = (pfx[seq] + split) * Hkv + kh; streamed range [t_begin, t_end)
-  // excludes the newest token of a fused-QKV step (not in the cache yet)
   auto item_of = [&](int idx) {
     Item it;
     const int u = idx / p.Hkv;
@@ -597,8 +521,6 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     const int ctx = p.ctx[it.seq];
     it.t_begin = it.split * p.split_tokens;
     it.t_end = min(ctx, it.t_begin + p.split_tokens);
-    it.has_new = fused && ctx - 1 >= it.t_begin && ctx - 1 < it.t_end;
-    if (it.has_new) it.t_end = ctx - 1;
     it.pg0 = it.t_begin >> 4;
     it.npg = it.t_end > it.t_begin ? ((it.t_end + 15) >> 4) - it.pg0 : 0;
     return it;
@@ -618,18 +540,22 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     if (lane == 31) s_wsum[warp] = incl;
     if (threadIdx.x == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+      // "done reading / writing" barriers take one arrival per thread of the
+      // releasing warp(s), so every thread's shared-memory accesses are
+      // ordered before the buffer's reuse (racecheck-clean); "data ready"
+      // barriers have one writer (or the TMA transaction count)
       for (int i = 0; i < R; ++i) {
         tc_mbar_init(&full[i], 1);
-        tc_mbar_init(&empty[i], 1);
+        tc_mbar_init(&empty[i], 32);
       }
       for (int i = 0; i < Q; ++i) {
         tc_mbar_init(&ifull[i], 1);
         tc_mbar_init(&qready[i], 1);
-        tc_mbar_init(&iempty[i], 1);
+        tc_mbar_init(&iempty[i], 32);
       }
       for (int i = 0; i < 2; ++i) {
-        tc_mbar_init(&oready[i], NWC);
-        tc_mbar_init(&ofree[i], 1);
+        tc_mbar_init(&oready[i], NWC * 32);
+        tc_mbar_init(&ofree[i], 32);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -645,9 +571,8 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   }
   __syncthreads();
   const int n_items = pfx[p.n] * p.Hkv;
-  // Every K / V page was written before this kernel started (this step's QKV
-  // epilogue writes only the newest token, which a fused step handles in the
-  // merge); nothing is read before the wait.
+  // Every K / V page, the newest token's included, and q were written by
+  // earlier kernels; nothing is read before the wait.
   pdl_wait();
 
   if (warp == NWC) {   // ---------------------------------------------------- producer
@@ -657,24 +582,45 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     // phases ahead even though the warps run items out of step.
     const uint64_t pol = l2_evict_first_policy();
     int c0 = 0, c1 = 0, c2 = 0, c3 = 0;   // pages issued per consumer warp
-    int next = 0;
-    if (lane == 0) next = atomicAdd(p.work, 1);
-    next = __shfl_sync(0xffffffffu, next, 0);
+    // Item indices are fetched two items ahead and the first 32 block-table
+    // entries of the next item are loaded while the current one streams, so
+    // neither the counter's nor the table's round trip stalls the ring.
+    auto fetch = [&]() {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(p.work, 1);
+      return v;
+    };
+    auto chunk0 = [&](int idx, Item& it) {
+      if (idx < 0) return 0;
+      it = item_of(idx);
+      const int32_t* bt = p.bt + (int64_t)it.seq * p.maxblk + it.pg0;
+      return lane < it.npg ? __ldg(bt + lane) : 0;
+    };
+    int cur = __shfl_sync(0xffffffffu, fetch(), 0);
+    cur = cur < n_items ? cur : -1;
+    int nxt = -1;
+    if (cur >= 0) {
+      nxt = __shfl_sync(0xffffffffu, fetch(), 0);
+      nxt = nxt < n_items ? nxt : -1;
+    }
+    Item it_cur{}, it_nxt{};
+    int bt_cur = chunk0(cur, it_cur), bt_nxt = chunk0(nxt, it_nxt);
     for (int n = 0;; ++n) {
-      const int idx = next < n_items ? next : -1;
+      const int idx = cur;
       const int q = n % Q;
       if (n >= Q) tc_mbar_wait(&iempty[q], ((uint32_t)(n / Q) & 1u) ^ 1u);
+      int pend = 0;
       if (lane == 0) {
         s_item[q] = idx;
         tc_mbar_arrive(&ifull[q]);
-        if (idx >= 0) next = atomicAdd(p.work, 1);
-        else pdl_trigger();   // no work left for this CTA: the next kernel may start its prologue
+        if (idx < 0) pdl_trigger();   // no work left for this CTA: the next kernel may start its prologue
+        else if (nxt >= 0) pend = atomicAdd(p.work, 1);
       }
       if (idx < 0) break;
-      const Item it = item_of(idx);
+      const Item it = it_cur;
       const int32_t* bt = p.bt + (int64_t)it.seq * p.maxblk + it.pg0;
       for (int j0 = 0; j0 < it.npg; j0 += 32) {
-        const int btv = j0 + lane < it.npg ? __ldg(bt + j0 + lane) : 0;
+        const int btv = j0 == 0 ? bt_cur : (j0 + lane < it.npg ? __ldg(bt + j0 + lane) : 0);
         const int cn = min(32, it.npg - j0);
         for (int j = 0; j < cn; ++j) {
           const int blk = __shfl_sync(0xffffffffu, btv, j);
@@ -695,26 +641,28 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           }
         }
       }
-      next = __shfl_sync(0xffffffffu, next, 0);
+      // rotate: the next item was fetched (and its table chunk loaded) one item ago
+      const int after = nxt >= 0 ? __shfl_sync(0xffffffffu, pend, 0) : -1;
+      cur = nxt;
+      it_cur = it_nxt;
+      bt_cur = bt_nxt;
+      nxt = after >= 0 && after < n_items ? after : -1;
+      bt_nxt = chunk0(nxt, it_nxt);
     }
   } else if (warp == NWC + 1) {   // ------------------------------------------ q-prep
     for (int n = 0;; ++n) {
       const int q = n % Q;
       tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u);
-      const int idx = s_item[q];
-      bf16* sq = qbuf + q * (G + 2) * HD;
+      int idx = 0;
+      if (lane == 0) idx = s_item[q];   // read by the lane whose qready arrival orders it
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      bf16* sq = qbuf + q * G * HD;
       if (idx < 0) {
         if (lane == 0) tc_mbar_arrive(&qready[q]);
         break;
       }
       const Item it = item_of(idx);
-      if (fused) {
-        fused_qkv_reduce<HD, G, 4>(p, it.seq, it.kh, p.ctx[it.seq] - 1, it.has_new, sq, lane, 32);
-        __syncwarp();
-        if (it.has_new) store_new_kv<HD, G>(p, it.seq, it.kh, p.ctx[it.seq] - 1, sq, lane);
-        __syncwarp();
-        if (lane == 0) tc_mbar_arrive(&qready[q]);
-      } else if (lane == 0) {
+      if (lane == 0) {
         tc_mbar_expect(&qready[q], G * HD * 2);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -730,7 +678,6 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       const int idx = s_item[q];
       if (idx < 0) break;
       const Item it = item_of(idx);
-      const bf16* sq = qbuf + q * (G + 2) * HD;
       tc_mbar_wait(&oready[b], (uint32_t)(n >> 1) & 1u);
       const float* so = obuf + b * (Lay::OBUF / 4);
       const float* sm = so + NWC * G * OS;      // [4][8]
@@ -754,28 +701,12 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           for (int w = 0; w < NWC; ++w) a += so[(w * G + g) * OS + dd * 32 + lane] * c[w];
           A[g][dd] = a;
         }
-        if (it.has_new) {   // the newest token (not streamed): score, then one online-softmax step
-          float sn = 0.f;
-          for (int e = lane; e < HD; e += 32) sn += __bfloat162float(sq[g * HD + e]) * __bfloat162float(sq[G * HD + e]);
-          sn = warp_sum(sn) * scale;
-          const float Mn = fmaxf(M, sn);
-          const float cm = M == -INFINITY ? 0.f : exp2f(M - Mn);
-          const float pn = exp2f(sn - Mn);
-          L = L * cm + pn;
-#pragma unroll
-          for (int dd = 0; dd < HD / 32; ++dd)
-            A[g][dd] = A[g][dd] * cm + pn * __bfloat162float(sq[(G + 1) * HD + dd * 32 + lane]);
-          M = Mn;
-        }
         Mg[g] = M;
         Lg[g] = L;
       }
       const Item itc = it;
-      __syncwarp();
-      if (lane == 0) {
-        tc_mbar_arrive(&ofree[b]);   // the consumers may reuse result buffer b
-        tc_mbar_arrive(&iempty[q]);  // queue slot q (descriptor, q buffer) free: the results are in registers
-      }
+      tc_mbar_arrive(&ofree[b]);    // the consumers may reuse result buffer b
+      tc_mbar_arrive(&iempty[q]);   // queue slot q (descriptor, q buffer) free: the results are in registers
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int h = itc.kh * G + g;
@@ -873,7 +804,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       const int idx = s_item[q];
       if (idx < 0) break;
       const Item it = item_of(idx);
-      const bf16* sq = qbuf + q * (G + 2) * HD;
+      const bf16* sq = qbuf + q * G * HD;
       // Q^T as the B operand of S^T = K Q^T: b0 = Q[head g][16j + 2t4 ..], b1 = [.. + 8]
       uint32_t qb[KS][2];
 #pragma unroll
@@ -924,8 +855,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           ldsm4_t(a, vt + page_off(v_row, 2 * d + v_ch));
           hmma16816(o[d], a, b0, b1);
         }
-        __syncwarp();
-        if (lane == 0) tc_mbar_arrive(&empty[s]);
+        tc_mbar_arrive(&empty[s]);   // this thread is done with the slot
       }
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
@@ -952,8 +882,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           so[(warp * G + h1) * OS + r0 + 8] = o[d][3];
         }
       }
-      __syncwarp();
-      if (lane == 0) tc_mbar_arrive(&oready[b]);
+      tc_mbar_arrive(&oready[b]);
     }
   }
   __syncthreads();
@@ -1009,7 +938,7 @@ static void launch_tc(const DecodeAttnParams& p, cudaStream_t st) {
 
 static bool use_tc(const DecodeAttnParams& p) {
   const int G = p.H / p.Hkv;
-  if (!p.kvmap || G > 8 || (p.hd != 64 && p.hd != 128) || p.impl == 1) return false;
+  if (!p.kvmap || p.qkv_ws || G > 8 || (p.hd != 64 && p.hd != 128) || p.impl == 1) return false;
   return G >= 2 || p.impl == 2;
 }
 

@@ -71,7 +71,7 @@ EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
            "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace",
-           "td_get_weight", "td_bench_step"]
+           "td_get_weight", "td_bench_step", "td_get_launch_bytes"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_run.argtypes = [C.c_void_p, P(td_run_stats)]
     lib.td_get_output.argtypes = [C.c_void_p, C.c_int64, P(C.c_int32), C.c_int32, P(C.c_int32)]
     lib.td_get_outputs.argtypes = [C.c_void_p, P(C.c_int32), C.c_int32, C.c_int32, P(C.c_int32)]
+    lib.td_get_launch_bytes.argtypes = [C.c_void_p, C.c_char_p, P(C.c_double), C.c_int64, P(C.c_int64)]
     lib.td_bench_step.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
                                   P(C.c_double)]
     lib.td_get_weight.argtypes = [C.c_void_p, C.c_int32, P(C.c_uint16), C.c_int64, P(C.c_int64), P(C.c_int64)]
@@ -254,6 +255,15 @@ class TDPipe:
         self._check(lib().td_bench_step(self.ctx, int(kind), int(n_seqs), int(length), int(iters), C.byref(us),
                                         C.byref(ideal)), "td_bench_step")
         return us.value, ideal.value
+
+    def td_get_launch_bytes(self, name: str) -> np.ndarray:
+        """Per-launch algorithmic bytes of kernel class `name` (timed runs), launch order."""
+        n = C.c_int64()
+        self._check(lib().td_get_launch_bytes(self.ctx, name.encode(), None, 0, C.byref(n)), "td_get_launch_bytes")
+        out = np.zeros(max(n.value, 1), dtype=np.float64)
+        self._check(lib().td_get_launch_bytes(self.ctx, name.encode(), _ptr(out, C.c_double), out.size, C.byref(n)),
+                    "td_get_launch_bytes")
+        return out[: n.value]
 
     def td_get_weight(self, tensor_id: int) -> np.ndarray:
         """bf16 bit patterns (uint16) of F9 tensor `tensor_id`, logical [rows, cols]."""

@@ -117,8 +117,12 @@ def projection(out, cfg, model, S, kv_cap=None):
     if not os.path.exists(prof):
         stage = dataclasses.replace(shape.with_layers(shape.n_layers // S), max_seq_len=4096)
         nb = (ctx_rep(wl) + 16) // 16 + 1
-        t = TDPipe(stage, 1, device=0, kv_blocks=1024 * nb + 64)
-        t.td_profile(prof, 1024, 2048, ctx_rep(wl))
+        lps = shape.n_layers // S
+        per_block = 2 * shape.n_kv_heads * 16 * shape.head_dim * 2 * lps
+        w_stage = HBM - RESERVE - stage_kv_blocks(shape, S) * per_block
+        b_max = int(min(1024, (HBM - RESERVE - w_stage - 8e9) // (nb * per_block)))
+        t = TDPipe(stage, 1, device=0, kv_blocks=b_max * nb + 64)
+        t.td_profile(prof, b_max, 2048, ctx_rep(wl))
         t.close()
     C = kv_cap or stage_kv_blocks(shape, S)
     big = dataclasses.replace(shape, max_seq_len=8192)

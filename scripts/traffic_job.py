@@ -6,13 +6,20 @@ printed for scripts/traffic_summary.py (same launches ncu saw; the schedule is
 the bench's -- C2 fits in HBM, so one prefill phase then decode; a synthetic
 frozen profile replaces td_profile so that no profiling launch is captured).
 
-    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:decode_attn --clock-control none \\
-        --csv --log-file gpurun_out/traffic_job.csv python scripts/traffic_job.py decode_attn > gpurun_out/traffic_job.json
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:decode_attn -s SKIP -c COUNT \\
+        --clock-control none --csv --log-file gpurun_out/traffic_w.csv python scripts/traffic_job.py decode_attn
+    python scripts/traffic_windows.py OUT.json SKIP:gpurun_out/traffic_w.csv [...]
+
+The per-launch algorithmic bytes (launch order) go to
+gpurun_out/traffic_job_<class>_bytes.npy so that a window of ncu-captured
+launches is compared with exactly the same launches.
 """
 import json
 import os
 import sys
 import tempfile
+
+import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2506_10470_b200 import TDPipe  # noqa: E402
@@ -28,6 +35,9 @@ t.td_upload()
 t.td_set_timing(True)
 st = t.td_run()
 k = t.td_get_timing(cls)
+per = t.td_get_launch_bytes(cls)
+np.save(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
+                     f"traffic_job_{cls}_bytes.npy"), per)
 t.close()
 print(json.dumps({"launches": k["launches"], "algorithmic_bytes": k["bytes"], "B": "C2 job (256 requests)",
                   "mean_ctx": None, "kernel_class": cls, "generated_tokens": st["generated_tokens"],
