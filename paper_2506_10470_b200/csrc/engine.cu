@@ -97,7 +97,7 @@ struct Meta {
   // [nd, n) are prefill chunks (q_start >= 0) of at most max_qlen tokens
   int hybrid = 0, nd = 0, max_qlen = 0;
   // offsets (in int32 units) into the packed buffer
-  int o_ctx, o_tokidx, o_pos, o_slot, o_seq, o_last, o_outpos, o_bt, o_qs;
+  int o_ctx, o_tokidx, o_pos, o_slot, o_seq, o_last, o_outpos, o_bt, o_qs, o_ord;
   int total = 0;
 };
 
@@ -522,7 +522,7 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   CK(cudaMalloc(&attn_cnt_, (n * Hkv_ + 2) * sizeof(int)));   // + the tensor-core kernel's work counters
   CK(cudaMemsetAsync(attn_cnt_, 0, (n * Hkv_ + 2) * sizeof(int), st_));
   // metadata ring: per seq 5 ints + bt, per token 4 ints, header
-  const int64_t need = 16 + 5 * n + 2 + n * maxblk + 4 * T + 64;
+  const int64_t need = 16 + 6 * n + 2 + n * maxblk + 4 * T + 64;
   if (need > meta_cap_) {
     for (int i = 0; i < kRing; ++i) {
       if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
@@ -577,13 +577,15 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
   int splits = 1;
   if (decode && T > 128) {
     // 129..512-token decode batches are near (or past) the tensor roof: the
-    // token-major kernel (128 tokens x 256 features per tile).  The residual
-    // GEMMs (O, down: their split partials are summed by the resid_norm launch
-    // that follows anyway) split K when their tiles fill the 148 SMs badly
-    // (< 96 tiles): the fewest splits giving >= 128 units, >= 16 k-blocks
-    // each.  Measured per shape in profiles/r2/gemm_sweep_t128.txt.
+    // token-major kernel (128 tokens x 256 features per tile, 128 features
+    // when that fills < 96 SMs).  The residual GEMMs (O, down: their split
+    // partials are summed by the resid_norm launch that follows anyway) split
+    // K when their tiles still fill the 148 SMs badly (< 96 tiles): the fewest
+    // splits giving >= 128 units, >= 16 k-blocks each.  Measured per shape in
+    // profiles/r2/gemm_sweep_t128.txt.
     decode = false;
-    const int64_t tiles = (int64_t)((T + 127) / 128) * ((N + 255) / 256);
+    const int fw = tnp_narrow(T, N) ? 128 : 256;
+    const int64_t tiles = (int64_t)((T + 127) / 128) * ((N + fw - 1) / fw);
     if (ep.mode == kEpiResid && defer && tiles < 96) {
       while (splits < 4 && tiles * splits < 128 && (K / 64) / (splits + 1) >= 16 &&
              (int64_t)(splits + 1) * T * ((N + 127) / 128 * 128) <= ws_cap_)
@@ -638,6 +640,7 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
   M.o_seq = off; off += T;
   M.o_bt = off; off += n * maxblk;
   M.o_qs = off; off += n;
+  M.o_ord = off; off += n;
   M.total = off;
   int32_t* h = hmeta_[r];
   int t = 0;
@@ -662,6 +665,11 @@ Meta CudaEngine::build_meta(int r, bool prefill, int n, const int* q_start, cons
     h[M.o_outpos + i] = emit && !emit[i] ? -1 : arena_off ? arena_off[i] + ctx : 0;
     h[M.o_qs + i] = q_start[i];
   }
+  // sequences by context length, longest first (the tensor-core decode
+  // attention numbers its work items in this order: longest-processing-first)
+  int32_t* ord = h + M.o_ord;
+  for (int i = 0; i < n; ++i) ord[i] = i;
+  std::stable_sort(ord, ord + n, [&](int32_t a, int32_t b) { return mb_ctx_[a] > mb_ctx_[b]; });
   return M;
 }
 
@@ -826,6 +834,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       dp.kvmap = have_kvmap_ ? &kvmap_ : nullptr;
       dp.layer = l - own_l0_;
       dp.work = attn_cnt_ + capN_ * Hkv_;
+      dp.order = dm + M.o_ord;
       if (defer_qkv && qsplits > 1) {
         dp.qkv_ws = ws_;
         dp.qkv_splits = qsplits;

@@ -504,7 +504,9 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   struct Item {
     int seq, kh, split, n_splits, t_begin, t_end, pg0, npg;
   };
-  // item idx = (pfx[seq] + split) * Hkv + kh; streamed range [t_begin, t_end)
+  // item idx = (pfx[r] + split) * Hkv + kh for the r-th sequence of p.order
+  // (longest context first: long items are taken first, short ones fill the
+  // tail); streamed range [t_begin, t_end)
   auto item_of = [&](int idx) {
     Item it;
     const int u = idx / p.Hkv;
@@ -515,7 +517,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       if (pfx[mid] <= u) lo = mid;
       else hi = mid - 1;
     }
-    it.seq = lo;
+    it.seq = p.order ? p.order[lo] : lo;
     it.split = u - pfx[lo];
     it.n_splits = pfx[lo + 1] - pfx[lo];
     const int ctx = p.ctx[it.seq];
@@ -530,7 +532,8 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     const int per = (p.n + kTcThreads - 1) / kTcThreads;
     const int i0 = min(p.n, (int)threadIdx.x * per), i1 = min(p.n, i0 + per);
     int sum = 0;
-    for (int i = i0; i < i1; ++i) sum += (p.ctx[i] + p.split_tokens - 1) / p.split_tokens;
+    auto ctx_at = [&](int i) { return p.ctx[p.order ? p.order[i] : i]; };
+    for (int i = i0; i < i1; ++i) sum += (ctx_at(i) + p.split_tokens - 1) / p.split_tokens;
     int incl = sum;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -565,7 +568,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     int run = base + incl - sum;
     for (int i = i0; i < i1; ++i) {
       pfx[i] = run;
-      run += (p.ctx[i] + p.split_tokens - 1) / p.split_tokens;
+      run += (ctx_at(i) + p.split_tokens - 1) / p.split_tokens;
     }
     if (threadIdx.x == kTcThreads - 1) pfx[p.n] = run;
   }

@@ -250,11 +250,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 // weight tile through L2); the two 256-column TMEM accumulators are double
 // buffered so the epilogue of tile i overlaps the MMAs of tile i+1, and the
 // smem ring runs continuously across tiles.
-template <int STAGES>
+template <int STAGES, int BNF>
 __global__ void __launch_bounds__(192, 1)
 gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int kb_total,
                 EpiParams ep, int nsplit, int kps, float* __restrict__ ws) {
-  constexpr int BNF = 256;
+  static_assert(BNF == 128 || BNF == 256, "feature tile: one or two 128-row packed weight tiles");
+  constexpr int WT = BNF / 128;
   constexpr int X_BYTES = 128 * BK * 2;
   constexpr int W_BYTES = BNF * BK * 2;
   constexpr int STAGE_BYTES = X_BYTES + W_BYTES;
@@ -306,9 +307,9 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
       bool waited = false;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int m0 = (tile % MT) * 128, nt = (tile / MT) % NT, ks = tile / (MT * NT);
-        const int wt0 = nt * 2;
-        const int n_wt = min(2, wtiles - wt0);
-        const uint32_t stage_tx = X_BYTES + n_wt * (W_BYTES / 2);
+        const int wt0 = nt * WT;
+        const int n_wt = min(WT, wtiles - wt0);
+        const uint32_t stage_tx = X_BYTES + n_wt * (W_BYTES / WT);
         for (int kb = ks * kps; kb < min(kb_total, (ks + 1) * kps); ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
@@ -316,8 +317,8 @@ gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict_
           uint8_t* sa = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], stage_tx);
           for (int h = 0; h < n_wt; ++h)
-            bulk_load(sa + X_BYTES + h * (W_BYTES / 2), wpk + (((int64_t)(wt0 + h) * kb_total + kb) << 13),
-                      W_BYTES / 2, &full[s], pol);
+            bulk_load(sa + X_BYTES + h * (W_BYTES / WT), wpk + (((int64_t)(wt0 + h) * kb_total + kb) << 13),
+                      W_BYTES / WT, &full[s], pol);
           if (!waited) {   // activations come from the previous kernel (PDL)
             pdl_wait();
             waited = true;
@@ -502,6 +503,8 @@ int tc_bn_for(int T, bool decode) {
   return 256;
 }
 
+bool tnp_narrow(int T, int N) { return (int64_t)((T + 127) / 128) * ((N + 255) / 256) < 96; }
+
 int effective_splits(int K, int splits) {
   const int kb_total = K / BK;
   const int kps = (kb_total + splits - 1) / splits;
@@ -512,20 +515,36 @@ int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const Epi
                    int* counters, bool decode, cudaStream_t st, bool defer_reduce) {
   if (T <= 0) return 1;
   if (!decode && W.packed && T > 128) {
-    // prefill: token-major tiles (vectorised epilogue), persistent
-    constexpr int STAGES = 4;
-    constexpr int sm = STAGES * (128 * BK * 2 + 256 * BK * 2) + 1024 + 256;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_tnp_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      attr = true;
-    }
+    // prefill / 129+-token decode: token-major tiles (vectorised epilogue),
+    // persistent; 128-feature tiles when 256-feature tiles fill < 96 SMs
     const int kb_total = W.K / BK;
     const int kps = (kb_total + std::max(splits, 1) - 1) / std::max(splits, 1);
     const int nsplit = (kb_total + kps - 1) / kps;
-    const int units = ((T + 127) / 128) * ((W.rows + 255) / 256) * nsplit;
-    launch_k(gemm_tnp_kernel<STAGES>, dim3(std::min(units, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T,
-             kb_total, ep, nsplit, kps, nsplit > 1 ? ws : nullptr);
+    const bool narrow = tnp_narrow(T, W.rows);
+    const int units = ((T + 127) / 128) * ((W.rows + (narrow ? 127 : 255)) / (narrow ? 128 : 256)) * nsplit;
+    auto go = [&](auto kern, int sm) {
+      launch_k(kern, dim3(std::min(units, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T, kb_total, ep,
+               nsplit, kps, nsplit > 1 ? ws : nullptr);
+    };
+    if (narrow) {
+      constexpr int STAGES = 6;
+      constexpr int sm = STAGES * (128 * BK * 2 + 128 * BK * 2) + 1024 + 256;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(gemm_tnp_kernel<STAGES, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        attr = true;
+      }
+      go(gemm_tnp_kernel<STAGES, 128>, sm);
+    } else {
+      constexpr int STAGES = 4;
+      constexpr int sm = STAGES * (128 * BK * 2 + 256 * BK * 2) + 1024 + 256;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(gemm_tnp_kernel<STAGES, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        attr = true;
+      }
+      go(gemm_tnp_kernel<STAGES, 256>, sm);
+    }
     if (nsplit > 1 && !defer_reduce) {
       const int64_t pairs = (int64_t)T * (W.rows / 2);
       const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);

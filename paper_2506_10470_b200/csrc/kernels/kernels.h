@@ -106,6 +106,7 @@ struct DecodeAttnParams {
   int layer = 0;
   int* work = nullptr;   // [2] zero-initialised work-item / done counters (re-armed by the kernel)
   int64_t n_items = 0;   // (sequence, split, kv head) items of the plan (plan_decode_attn)
+  const int32_t* order = nullptr;   // [n] sequences longest-first for the tensor-core kernel's items (nullable)
   int impl = 0;          // 0: kernel by shape (tensor cores for GQA hd 64/128); 1: SIMT; 2: tensor cores (td_bench_attn)
 };
 // 3-D TMA descriptor of a KV pool [n_layers][C blocks][K|V][Hkv][16][hd] bf16

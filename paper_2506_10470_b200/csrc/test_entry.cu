@@ -172,14 +172,14 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
   const int cap = (max_ctx + kAttnMinSplitGQA - 1) / kAttnMinSplitGQA;   // any launch plan fits
   bf16 *kv = nullptr, *q = nullptr, *o = nullptr;
   float* part = nullptr;
-  int32_t *dctx = nullptr, *dbt = nullptr;
+  int32_t *dctx = nullptr, *dbt = nullptr, *dord = nullptr;
   int* cnt = nullptr;
   td_status st = TD_OK;
   cudaStream_t s;
   cudaStreamCreate(&s);
   if (cudaMalloc(&kv, pool * blk_bytes) || cudaMalloc(&q, (size_t)n * H * hd * 2) ||
       cudaMalloc(&o, (size_t)n * H * hd * 2) || cudaMalloc(&part, (size_t)n * H * cap * (hd + 2) * 4) ||
-      cudaMalloc(&dctx, n * 4) || cudaMalloc(&dbt, bt.size() * 4) ||
+      cudaMalloc(&dctx, n * 4) || cudaMalloc(&dbt, bt.size() * 4) || cudaMalloc(&dord, n * 4) ||
       cudaMalloc(&cnt, ((size_t)n * Hkv + 2) * 4)) {
     st = TD_ENOMEM;
   } else {
@@ -188,9 +188,14 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
     cudaMemset(cnt, 0, ((size_t)n * Hkv + 2) * 4);
     cudaMemcpy(dctx, ctx, n * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice);
+    std::vector<int32_t> ord(n);   // longest context first, as the engine's metadata
+    for (int i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return ctx[a] > ctx[b]; });
+    cudaMemcpy(dord, ord.data(), n * 4, cudaMemcpyHostToDevice);
     DecodeAttnParams p{q, kv, dctx, dbt, maxblk, o, part, 0, n, H, Hkv, hd, 0, cnt};
     p.part_cap = (int64_t)n * cap;
     p.work = cnt + (size_t)n * Hkv;
+    p.order = dord;
     CUtensorMap kvmap;
     if (hd >= 64 && make_kv_map(&kvmap, kv, pool, Hkv, hd, 1)) p.kvmap = &kvmap;
     p.impl = impl;
@@ -221,7 +226,7 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
     cudaEventDestroy(b);
   }
   cudaFree(kv); cudaFree(q); cudaFree(o); cudaFree(part);
-  cudaFree(dctx); cudaFree(dbt); cudaFree(cnt);
+  cudaFree(dctx); cudaFree(dbt); cudaFree(dord); cudaFree(cnt);
   cudaStreamDestroy(s);
   return st;
 }

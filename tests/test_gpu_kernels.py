@@ -33,11 +33,14 @@ def test_gemm_vs_fp64(T, N, K, impl, splits):
 
 
 @pytest.mark.parametrize("T,N,K,splits", [(129, 256, 1024, 2), (256, 1024, 4096, 3), (300, 640, 576, 2),
-                                          (512, 4096, 2048, 4), (200, 384, 512, 8), (256, 8192, 1024, 1)])
+                                          (512, 4096, 2048, 4), (200, 384, 512, 8), (256, 8192, 1024, 1),
+                                          (2048, 4096, 512, 1), (1900, 3200, 256, 2), (640, 12288, 192, 3)])
 def test_gemm_token_major_split_k_vs_fp64(T, N, K, splits):
     """The persistent token-major tcgen05 kernel with split-K (impl 4): every
     split writes an fp32 partial tile, reduced in split order -- the engine's
-    path for 129..512-token decode micro-batches; bitwise repeatable."""
+    path for 129..512-token decode micro-batches; 128-feature tiles when the
+    256-feature tiles fill < 96 SMs, 256 otherwise (the last three cases);
+    bitwise repeatable."""
     rng = np.random.default_rng(T * 13 + N + K + splits)
     Ab, Af = _bf16(rng, (T, K))
     Wb, Wf = _bf16(rng, (N, K), 1.0 / np.sqrt(K))
