@@ -577,15 +577,13 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
   int splits = 1;
   if (decode && T > 128) {
     // 129..512-token decode batches are near (or past) the tensor roof: the
-    // token-major kernel (128 tokens x 256 features per tile, 128 features
-    // when that fills < 96 SMs).  The residual GEMMs (O, down: their split
-    // partials are summed by the resid_norm launch that follows anyway) split
-    // K when their tiles still fill the 148 SMs badly (< 96 tiles): the fewest
-    // splits giving >= 128 units, >= 16 k-blocks each.  Measured per shape in
-    // profiles/r2/gemm_sweep_t128.txt.
+    // token-major kernel (128 tokens x 256 features per tile).  The residual
+    // GEMMs (O, down: their split partials are summed by the resid_norm launch
+    // that follows anyway) split K when their tiles fill the 148 SMs badly
+    // (< 96 tiles): the fewest splits giving >= 128 units, >= 16 k-blocks
+    // each.  Measured per shape in profiles/r2/gemm_sweep_t128.txt.
     decode = false;
-    const int fw = tnp_narrow(T, N) ? 128 : 256;
-    const int64_t tiles = (int64_t)((T + 127) / 128) * ((N + fw - 1) / fw);
+    const int64_t tiles = (int64_t)((T + 127) / 128) * ((N + 255) / 256);
     if (ep.mode == kEpiResid && defer && tiles < 96) {
       while (splits < 4 && tiles * splits < 128 && (K / 64) / (splits + 1) >= 16 &&
              (int64_t)(splits + 1) * T * ((N + 127) / 128 * 128) <= ws_cap_)

@@ -254,7 +254,7 @@ template <int STAGES, int BNF>
 __global__ void __launch_bounds__(192, 1)
 gemm_tnp_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ wpk, int Nf, int T, int kb_total,
                 EpiParams ep, int nsplit, int kps, float* __restrict__ ws) {
-  static_assert(BNF == 128 || BNF == 256, "feature tile: one or two 128-row packed weight tiles");
+  static_assert(BNF == 128 || BNF == 256, "feature tile: one or two 128-row packed weight tiles");   // 256 in use
   constexpr int WT = BNF / 128;
   constexpr int X_BYTES = 128 * BK * 2;
   constexpr int W_BYTES = BNF * BK * 2;
@@ -503,8 +503,6 @@ int tc_bn_for(int T, bool decode) {
   return 256;
 }
 
-bool tnp_narrow(int T, int N) { return (int64_t)((T + 127) / 128) * ((N + 255) / 256) < 96; }
-
 int effective_splits(int K, int splits) {
   const int kb_total = K / BK;
   const int kps = (kb_total + splits - 1) / splits;
@@ -516,35 +514,22 @@ int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const Epi
   if (T <= 0) return 1;
   if (!decode && W.packed && T > 128) {
     // prefill / 129+-token decode: token-major tiles (vectorised epilogue),
-    // persistent; 128-feature tiles when 256-feature tiles fill < 96 SMs
+    // persistent.  (128-feature tiles for under-filled grids were measured
+    // slower in context: twice the activation re-reads per FLOP,
+    // profiles/r2/gemm_sweep_t128.txt)
+    constexpr int STAGES = 4;
+    constexpr int sm = STAGES * (128 * BK * 2 + 256 * BK * 2) + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_tnp_kernel<STAGES, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      attr = true;
+    }
     const int kb_total = W.K / BK;
     const int kps = (kb_total + std::max(splits, 1) - 1) / std::max(splits, 1);
     const int nsplit = (kb_total + kps - 1) / kps;
-    const bool narrow = tnp_narrow(T, W.rows);
-    const int units = ((T + 127) / 128) * ((W.rows + (narrow ? 127 : 255)) / (narrow ? 128 : 256)) * nsplit;
-    auto go = [&](auto kern, int sm) {
-      launch_k(kern, dim3(std::min(units, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base, W.rows, T, kb_total, ep,
-               nsplit, kps, nsplit > 1 ? ws : nullptr);
-    };
-    if (narrow) {
-      constexpr int STAGES = 6;
-      constexpr int sm = STAGES * (128 * BK * 2 + 128 * BK * 2) + 1024 + 256;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(gemm_tnp_kernel<STAGES, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        attr = true;
-      }
-      go(gemm_tnp_kernel<STAGES, 128>, sm);
-    } else {
-      constexpr int STAGES = 4;
-      constexpr int sm = STAGES * (128 * BK * 2 + 256 * BK * 2) + 1024 + 256;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(gemm_tnp_kernel<STAGES, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        attr = true;
-      }
-      go(gemm_tnp_kernel<STAGES, 256>, sm);
-    }
+    const int units = ((T + 127) / 128) * ((W.rows + 255) / 256) * nsplit;
+    launch_k(gemm_tnp_kernel<STAGES, 256>, dim3(std::min(units, 148)), dim3(192), sm, st, Xby_bn[2].map, W.base,
+             W.rows, T, kb_total, ep, nsplit, kps, nsplit > 1 ? ws : nullptr);
     if (nsplit > 1 && !defer_reduce) {
       const int64_t pairs = (int64_t)T * (W.rows / 2);
       const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);

@@ -20,9 +20,6 @@ bool make_tc_operand(TcOperand* op, const bf16* base, int rows, int K, int box_r
 // A tile-packed weight operand [rows (padded to 128), K]: no tensor map needed.
 TcOperand packed_weight(const bf16* base, int rows, int K);
 int tc_bn_for(int T, bool decode);
-// the token-major kernel (T > 128) uses 128-feature tiles when 256-feature
-// tiles would fill fewer than 96 SMs
-bool tnp_narrow(int T, int N);
 // out = X[T, K] . W[Nf, K]^T with epilogue ep.  Xby_bn[i] = X described with
 // box rows 32 << i.  splits > 1: split-K through workspace ws
 // [tiles][splits][128][BN] fp32 and zero-initialised per-tile counters.
