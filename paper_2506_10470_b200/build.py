@@ -42,6 +42,8 @@ NCCL_INC = _nccl_include()
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + (["-I" + NCCL_INC] if NCCL_INC else ["-DTDP_NO_NCCL"])
 CU_FLAGS = ARCH + ["-Xptxas", "-v", "--expt-relaxed-constexpr", "-diag-suppress", "177"]
+# extra -D flags for A/B builds of compile-time tuning constants (measurement only)
+COMMON += os.environ.get("TDP_NVCC_DEFINES", "").split()
 
 
 def sources():

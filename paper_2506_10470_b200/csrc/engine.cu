@@ -753,7 +753,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
   // Decode attention is launched without PDL (a PDL dependent, it made decode
   // steps 2-10 % slower at b >= 8: profiles/r1/pdl_ab.md); every other hot
   // kernel is a PDL dependent of its predecessor.
-  const bool attn_nopdl = !M.prefill;
+  const bool attn_nopdl = !M.prefill && M.n > kAttnPdlMaxN;
   const int T = M.T, n = M.n;
   const int nqkv = (H_ + 2 * Hkv_) * hd_;
   const float eps = s_.rms_eps;

@@ -507,6 +507,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   // item idx = (pfx[r] + split) * Hkv + kh for the r-th sequence of p.order
   // (longest context first: long items are taken first, short ones fill the
   // tail); streamed range [t_begin, t_end)
+  __shared__ Item s_desc[Q];   // the queued items, decoded once by the producer
   auto item_of = [&](int idx) {
     Item it;
     const int u = idx / p.Hkv;
@@ -615,6 +616,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       int pend = 0;
       if (lane == 0) {
         s_item[q] = idx;
+        if (idx >= 0) s_desc[q] = it_cur;
         tc_mbar_arrive(&ifull[q]);
         if (idx < 0) pdl_trigger();   // no work left for this CTA: the next kernel may start its prologue
         else if (nxt >= 0) pend = atomicAdd(p.work, 1);
@@ -664,8 +666,8 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
         if (lane == 0) tc_mbar_arrive(&qready[q]);
         break;
       }
-      const Item it = item_of(idx);
       if (lane == 0) {
+        const Item it = s_desc[q];
         tc_mbar_expect(&qready[q], G * HD * 2);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -680,7 +682,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u);
       const int idx = s_item[q];
       if (idx < 0) break;
-      const Item it = item_of(idx);
+      const Item it = s_desc[q];
       tc_mbar_wait(&oready[b], (uint32_t)(n >> 1) & 1u);
       const float* so = obuf + b * (Lay::OBUF / 4);
       const float* sm = so + NWC * G * OS;      // [4][8]
@@ -806,7 +808,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       tc_mbar_wait(&qready[q], (uint32_t)(n / Q) & 1u);
       const int idx = s_item[q];
       if (idx < 0) break;
-      const Item it = item_of(idx);
+      const Item it = s_desc[q];
       const bf16* sq = qbuf + q * G * HD;
       // Q^T as the B operand of S^T = K Q^T: b0 = Q[head g][16j + 2t4 ..], b1 = [.. + 8]
       uint32_t qb[KS][2];
@@ -1020,17 +1022,21 @@ void plan_decode_attn(DecodeAttnParams& p, const int* ctx) {
   p.n_items = ctas_at(split);
 }
 
-// Decode attention is never a PDL dependent: the SIMT kernel issues its first
-// K / V loads before griddepcontrol.wait, which is only safe because the
-// launch waits for its predecessor in the ordinary way; the
-// suppression is enforced here, not left to the caller.
+// Decode attention is a PDL dependent only for batches of <= kAttnPdlMaxN
+// sequences (SIMT kernel).  Its first K / V loads go out before
+// griddepcontrol.wait; that is safe because every K / V page it reads
+// early was written by an earlier micro-batch, and consecutive micro-batches
+// are separated by their metadata H2D copy (a non-kernel stream operation,
+// which PDL never overlaps); the newest token is re-read after the wait.
+// Larger batches wait for their predecessor in the ordinary way (measured
+// faster, profiles/r1/pdl_ab.md).  Enforced here, not left to the caller.
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {
   if (p.n <= 0) return;
   struct NoPdl {
     bool prev;
-    NoPdl() : prev(!pdl_enabled()) { pdl_suppress(true); }
+    explicit NoPdl(bool on) : prev(!pdl_enabled()) { pdl_suppress(on || prev); }
     ~NoPdl() { pdl_suppress(prev); }
-  } no_pdl;
+  } no_pdl(p.n > kAttnPdlMaxN || use_tc(p));
   switch (p.hd) {
     case 16: launch_decode_hd<16>(p, st); break;
     case 32: launch_decode_hd<32>(p, st); break;

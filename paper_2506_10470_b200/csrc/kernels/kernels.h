@@ -123,6 +123,10 @@ constexpr int kAttnMinSplit = 128;   // 64 measured slower (profiles/r1/optimisa
 // DecodeAttnParams::part_cap (the engine sizes part[] for kAttnSmallN sequences
 // at 32-token splits)
 constexpr int kAttnMinSplitGQA = 32;
+#ifndef TDP_ATTN_PDL_MAXN
+#define TDP_ATTN_PDL_MAXN 0
+#endif
+constexpr int kAttnPdlMaxN = TDP_ATTN_PDL_MAXN;   // decode attention as a PDL dependent up to this batch size
 constexpr int kAttnSmallN = 32;
 void plan_decode_attn(DecodeAttnParams& p, const int* ctx_host);
 
