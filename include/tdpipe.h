@@ -124,6 +124,12 @@ typedef struct td_options {
   /* roofline accounting (td_run_stats.ideal_ns): peaks of this device; 0 = off */
   double hbm_peak_gbs;          /* HBM bandwidth, GB/s (measured copy bandwidth)        */
   double tc_peak_tflops;        /* dense bf16 tensor-core TFLOP/s                       */
+  /* execution plan of decode micro-batches of <= 128 tokens (same results up to
+     fp32 summation order) */
+  int32_t decode_chain;         /* 0 (default): one kernel per GEMM / reduction (PDL);
+                                   1: one persistent kernel per layer for the weight
+                                   GEMMs + reductions, attention separate (measured
+                                   1-10 % slower: profiles/r2/chain/)               */
 } td_options;
 
 typedef struct td_run_stats {
@@ -300,11 +306,25 @@ td_status td_get_launch_bytes(struct td_ctx* ctx, const char* name, double* out,
  * W through a TMA descriptor; splits > 1 exercises the split-K reduction
  * (T > 128 with impl 0 and splits == 1: the persistent token-major prefill
  * kernel); impl 4 = the token-major kernel with `splits` K splits (T > 128;
- * the engine's path for 129+-token decode micro-batches).  Runs on `device`,
+ * the engine's path for 129+-token decode micro-batches); impl 5 = the
+ * persistent decode chain (decode_chain.cu) on one GEMM op whose weight tiles
+ * are reduced into a zeroed residual (T <= 128, N % 128 == 0).  Runs on `device`,
  * allocates and frees its own buffers, synchronous.  TD_EINVAL for any other
  * impl. */
 td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N, int32_t K,
                        int32_t impl, int32_t splits, float* out);
+
+/* The persistent decode chain (decode_chain.cu) on one MLP block (testing
+ * only): a = bf16(RMSNorm(x0) * g), h = bf16(silu(Wgu[2j] . a) * (Wgu[2j+1] . a)),
+ * x = x0 + Wd . h -- the chain ops residual + norm, GEMM, SwiGLU, GEMM,
+ * residual with grid barriers between them.  x0 [T, d] fp32;
+ * g [d], Wgu [2F, d] (gate / up rows interleaved), Wd [d, F] bf16 bit
+ * patterns; outputs a [T, d] and h [T, F] (bf16 bits) and x [T, d] fp32,
+ * host buffers owned by the caller.  T in [1, 128], d and F multiples of 64;
+ * TD_EINVAL otherwise.  Allocates and frees its own device buffers, synchronous. */
+td_status td_test_chain_mlp(int32_t device, const float* x0, const uint16_t* g, const uint16_t* Wgu,
+                            const uint16_t* Wd, int32_t T, int32_t d, int32_t F, float eps, uint16_t* a_out,
+                            uint16_t* h_out, float* x_out);
 
 /* GEMM timing sweep (testing only): average device microseconds per call of
  * the tcgen05 GEMM on [T, K] x [N, K]^T (tile-packed weights, fp32 output),

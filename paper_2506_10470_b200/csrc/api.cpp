@@ -82,6 +82,7 @@ extern "C" void td_default_options(td_options* o) {
   o->allgather_user = nullptr;
   o->hbm_peak_gbs = 0.0;
   o->tc_peak_tflops = 0.0;
+  o->decode_chain = 0;
 }
 
 static bool read_profile(const std::string& path, std::vector<int64_t>* tdec, std::vector<int64_t>* tpre,

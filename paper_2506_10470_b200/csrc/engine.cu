@@ -149,6 +149,9 @@ class CudaEngine : public Engine {
                   const std::vector<const std::vector<int32_t>*>& blocks, const int32_t* bt_flat, int bt_stride);
   td_status run_stage(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena, float* xpeer = nullptr,
                       bool* sent = nullptr);
+  td_status run_stage_chain(int stage, const Meta& M, const int32_t* dmeta, int32_t* arena, float* xpeer,
+                            bool* sent);
+  void launch_chain(ChainProgram& P, int T, int sub_cls);
   td_status run_microbatch(const Meta& M, const int32_t* dmeta, int32_t* arena);
   td_status make_x_ops();
   int gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, const EpiParams& ep, bool decode,
@@ -215,6 +218,14 @@ class CudaEngine : public Engine {
   XOps xa_, xo_, xh_;
   float* ws_ = nullptr;
   int64_t ws_cap_ = 0;
+  // persistent decode-layer chain (decode_chain.cu): grid = SM count
+  int nsm_ = 148;
+  bool chain_ok_ = false;
+  unsigned long long* chain_bar_ = nullptr;   // grid-barrier counter
+  uint64_t chain_base_ = 0;                   // its value after every enqueued chain launch
+  float* ssq_ = nullptr;                      // [128][kChainSsqStride] per-tile sums of squares
+  int* tile_cnt_ = nullptr;                   // [2][kChainMaxTiles] per-tile arrival counters
+  int chain_parity_ = 0;                      // counter buffer of the next chain launch's first GEMM
   int* counters_ = nullptr;
   int* attn_cnt_ = nullptr;   // decode-attention split tickets [capN * Hkv]
   std::vector<int> mb_ctx_;   // context length per sequence of the micro-batch being enqueued
@@ -257,7 +268,7 @@ class CudaEngine : public Engine {
                                       "gemm_o_dec", "gemm_gu_dec", "gemm_down_dec", "lm_head_dec",
                                       "decode_attn@b1-8", "decode_attn@b9-32", "decode_attn@b33-128",
                                       "decode_attn@b129+", "gemm_dec@b1-8", "gemm_dec@b9-32", "gemm_dec@b33-128",
-                                      "gemm_dec@b129+"};
+                                      "gemm_dec@b129+", "decode_chain"};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev_;
   // trace of a timed run: (micro-batch, kind, stage, timed_ index of its span),
   // (timed_ index of the micro-batch's first span, KV blocks in use at launch)
@@ -272,7 +283,8 @@ class CudaEngine : public Engine {
 enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
 constexpr int kSkTicketOff = 1 << 15;   // counters_[kSkTicketOff ..]: stream-K GEMM tile tickets
 constexpr int kDecOff = 8;   // decode-phase GEMM classes = prefill class + kDecOff
-constexpr int kAttnBucket = 15, kGemmBucket = 19;   // + bucket(n): batch-size buckets for decode
+constexpr int kAttnBucket = 15, kGemmBucket = 19;
+constexpr int cChain = 23;   // the persistent decode-layer chain (T <= 128)   // + bucket(n): batch-size buckets for decode
 static inline int bucket_of(int n) { return n <= 8 ? 0 : n <= 32 ? 1 : n <= 128 ? 2 : 3; }
 
 // --------------------------------------------------------------------- init
@@ -296,6 +308,7 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, dev_));
   if (prop.major != 10) { error = "needs an sm_100 (B200) device"; return TD_ECUDA; }
+  nsm_ = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   // layer partition: balanced, remainder to earlier stages
   int q = s.n_layers / S_, r = s.n_layers % S_, l = 0;
@@ -450,6 +463,17 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
                                                     (int64_t)o.max_batch_seqs + std::max(o.hb_tokens, 0)}),
                                  (int64_t)o.max_batch_seqs + std::max(o.hb_tokens, 0)))
       return e3;
+  // the decode chain: shapes whose GEMM dims are whole 64-wide k blocks
+  chain_ok_ = o.decode_chain != 0 && d_ % 128 == 0 && d_ / 128 <= kChainSsqStride && F_ % 64 == 0 &&
+              cdiv(2LL * F_, 128) <= kChainMaxTiles && cdiv((int64_t)(H_ + 2 * Hkv_) * hd_, 128) <= kChainMaxTiles &&
+              (H_ * hd_) % 64 == 0;
+  CK(cudaMalloc(&chain_bar_, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(chain_bar_, 0, sizeof(unsigned long long), st_));
+  chain_base_ = 0;
+  CK(cudaMalloc(&ssq_, 128 * kChainSsqStride * sizeof(float)));
+  CK(cudaMalloc(&tile_cnt_, 2 * kChainMaxTiles * sizeof(int)));
+  CK(cudaMemsetAsync(tile_cnt_, 0, 2 * kChainMaxTiles * sizeof(int), st_));
+  chain_parity_ = 0;
   CK(cudaEventCreate(&ev_start_));
   CK(cudaEventCreate(&ev_end_));
   for (int i = 0; i < kRing; ++i) CK(cudaEventCreateWithFlags(&ring_ev_[i], cudaEventDisableTiming));
@@ -474,6 +498,9 @@ void CudaEngine::release() {
   cudaFree(arena_);
   cudaFree(ws_);
   cudaFree(counters_);
+  cudaFree(chain_bar_);
+  cudaFree(ssq_);
+  cudaFree(tile_cnt_);
   cudaFree(attn_cnt_);
   for (int i = 0; i < kRing; ++i) {
     if (hmeta_[i]) cudaFreeHost(hmeta_[i]);
@@ -541,7 +568,10 @@ td_status CudaEngine::ensure_work(int64_t T, int64_t n, int64_t maxblk) {
   capN_ = n;
   capBlk_ = maxblk;
   // split-K workspace (L2-resident partial tiles) + per-tile tickets
-  const int64_t wneed = 16LL << 20;   // 64 MB of fp32; gemm() falls back to fewer splits beyond it
+  // 64 MB of fp32 (gemm() falls back to fewer splits beyond it), and at least
+  // the decode chain's segment partials of its widest GEMM at 128 tokens
+  const int64_t max_tiles = cdiv(std::max<int64_t>({2LL * F_, (int64_t)(H_ + 2 * Hkv_) * hd_, (int64_t)d_}), 128);
+  const int64_t wneed = std::max<int64_t>(16LL << 20, (max_tiles + nsm_) * 128 * 128);
   if (wneed > ws_cap_) {
     cudaFree(ws_);
     CK(cudaMalloc(&ws_, wneed * 4));
@@ -749,6 +779,7 @@ bool CudaEngine::get_timing(const std::string& name, KernelTiming* t) {
 // ------------------------------------------------------------------ forward
 td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int32_t* arena, float* xpeer,
                                 bool* sent) {
+  if (chain_ok_ && !M.prefill && !M.hybrid && M.T <= 128) return run_stage_chain(stage, M, dm, arena, xpeer, sent);
   if (sent) *sent = false;
   // Decode attention is launched without PDL (a PDL dependent, it made decode
   // steps 2-10 % slower at b >= 8: profiles/r1/pdl_ab.md); every other hot
@@ -894,6 +925,150 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     el.ldo = V_;
     const int il = tbegin(cLM + (M.prefill ? 0 : kDecOff));
     gemm(xa_, tlm_, n, V_, d_, el, dec);
+    tend(il, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
+    launches_++;
+    if (arena) {
+      launch_argmax(logits_, n, V_, arena, dm + M.o_outpos, st_);
+      launches_++;
+    }
+  }
+  return TD_OK;
+}
+
+// One chain launch (decode_chain.cu); the timed span counts the algorithmic
+// bytes / FLOPs of its GEMMs (weights + activations in and out).
+void CudaEngine::launch_chain(ChainProgram& P, int T, int sub_cls) {
+  P.T = T;
+  P.d = d_;
+  P.eps = s_.rms_eps;
+  P.ws = ws_;
+  P.ssq = ssq_;
+  P.cnt = tile_cnt_;
+  P.cnt_parity = chain_parity_;
+  P.bar = chain_bar_;
+  P.bar_base = chain_base_;
+  P.trace_on = P.n_ops >= 4;   // (trace builds) a full post-attention layer program
+  double bytes = 0, flops = 0;
+  for (int i = 0; i < P.n_ops; ++i)
+    if (P.op[i].kind == kChGemm) {
+      const double N = P.op[i].N, K = P.op[i].K;
+      bytes += N * K * 2 + (double)T * K * 2 + (double)T * N * 2;
+      flops += 2.0 * T * N * K;
+    }
+  const int bi = T <= 32 ? 0 : T <= 64 ? 1 : 2;
+  const CUtensorMap maps[3] = {xa_.by_bn[bi].map, xo_.by_bn[bi].map, xh_.by_bn[bi].map};
+  const int it = tbegin(cChain);
+  if (it >= 0) timed_[it].sub = sub_cls;
+  launch_decode_chain(P, maps, nsm_, st_);
+  tend(it, bytes, flops);
+  chain_base_ += (uint64_t)nsm_ * chain_barriers(P);
+  chain_parity_ = (chain_parity_ + chain_gemms(P)) & 1;
+  launches_++;
+}
+
+// Decode micro-batch of <= 128 tokens: per layer one attention launch and one
+// persistent chain launch covering  O-proj -> residual + RMSNorm -> gate/up ->
+// SwiGLU -> down -> residual (+ the stage hand-off store) -> the next layer's
+// RMSNorm -> QKV -> RoPE + K/V write.  Same arithmetic as run_stage up to the
+// fp32 summation order of the split-K partials and norm sums.
+td_status CudaEngine::run_stage_chain(int stage, const Meta& M, const int32_t* dm, int32_t* arena, float* xpeer,
+                                      bool* sent) {
+  if (sent) *sent = false;
+  const int T = M.T, n = M.n;
+  const int nqkv = (H_ + 2 * Hkv_) * hd_;
+  const int sub = kGemmBucket + bucket_of(T);
+  if (stage == 0) {
+    launch_embed(arena, dm + M.o_tokidx, E_, x_, T, d_, st_);
+    launches_++;
+  }
+  auto add = [](ChainProgram& P, const ChainOp& op) { P.op[P.n_ops++] = op; };
+  auto gemm_op = [](const TcOperand& W, int N, int K, int xmap, int red) {
+    ChainOp g{};
+    g.kind = kChGemm;
+    g.red = red;
+    g.w = W.base;
+    g.N = N;
+    g.K = K;
+    g.xmap = xmap;
+    return g;
+  };
+  // residual GEMMs (O, down): x += W.X (+ the hand-off store); a = bf16(x * g)
+  // and the sums of squares for the next GEMM's RMSNorm when g != nullptr
+  auto resid_gemm = [&](const TcOperand& W, int K, int xmap, float* xp, const bf16* g) {
+    ChainOp r = gemm_op(W, d_, K, xmap, kRedResid);
+    r.x = x_;
+    r.xpeer = xp;
+    r.g = g;
+    r.out = a_;
+    return r;
+  };
+  auto qkv_op = [&](int l) {
+    ChainOp r = gemm_op(L_[l].tqkv, nqkv, d_, 0, kRedQKV);
+    EpiParams& ep = r.ep;
+    ep.mode = kEpiQKV;
+    ep.out_bf16 = q_;
+    ep.kcache = kv_ + (int64_t)(l - own_l0_) * C_ * (kv_block_bytes_layer_ / 2);
+    ep.pos = dm + M.o_pos;
+    ep.slot = dm + M.o_slot;
+    ep.rope_cs = rope_;
+    ep.H = H_;
+    ep.Hkv = Hkv_;
+    ep.hd = hd_;
+    return r;
+  };
+  const int l0 = stage_l0_[stage], l1 = stage_l1_[stage];
+  {
+    ChainProgram P{};
+    ChainOp pr{};
+    pr.kind = kChPrep;   // a = bf16(x * g1), sums of squares of x
+    pr.x = x_;
+    pr.g = L_[l0].g1;
+    pr.out = a_;
+    add(P, pr);
+    add(P, qkv_op(l0));
+    launch_chain(P, T, sub);
+  }
+  for (int l = l0; l < l1; ++l) {
+    const LayerW& w = L_[l];
+    bf16* kvl = kv_ + (int64_t)(l - own_l0_) * C_ * (kv_block_bytes_layer_ / 2);
+    DecodeAttnParams dp{q_, kvl, dm + M.o_ctx, dm + M.o_bt, M.maxblk, ob_, part_, 0, n, H_, Hkv_, hd_, 0, attn_cnt_};
+    dp.part_cap = part_cap_;
+    dp.kvmap = have_kvmap_ ? &kvmap_ : nullptr;
+    dp.layer = l - own_l0_;
+    dp.work = attn_cnt_ + capN_ * Hkv_;
+    dp.order = dm + M.o_ord;
+    plan_decode_attn(dp, mb_ctx_.data());
+    const int ida = tbegin(cDecAttn);
+    if (ida >= 0) timed_[ida].sub = kAttnBucket + bucket_of(n);
+    pdl_suppress(n > kAttnPdlMaxN);
+    launch_decode_attn(dp, st_);
+    pdl_suppress(false);
+    tend(ida, 0, 0);
+    launches_++;
+    const bool last = l + 1 == l1;
+    ChainProgram P{};
+    add(P, resid_gemm(w.to, H_ * hd_, 1, nullptr, w.g2));
+    {
+      ChainOp gu = gemm_op(w.tgu, 2 * F_, d_, 0, kRedSwiGLU);
+      gu.out = h_;
+      add(P, gu);
+    }
+    // the stage's final residual rows also go straight into the next stage's
+    // receive slot (peer store over NVLink; no separate send)
+    add(P, resid_gemm(w.td, F_, 2, last ? xpeer : nullptr, last ? nullptr : L_[l + 1].g1));
+    if (last && xpeer && sent) *sent = true;
+    if (!last) add(P, qkv_op(l + 1));
+    launch_chain(P, T, sub);
+  }
+  if (stage == S_ - 1) {
+    launches_++;   // final norm
+    launch_rmsnorm(x_, gf_, a_, dm + M.o_last, n, d_, s_.rms_eps, st_);
+    EpiParams el{};
+    el.mode = kEpiF32;
+    el.out_f32 = logits_;
+    el.ldo = V_;
+    const int il = tbegin(cLM + kDecOff);
+    gemm(xa_, tlm_, n, V_, d_, el, true);
     tend(il, (double)V_ * d_ * 2 + (double)n * d_ * 2 + 4.0 * n * V_, 2.0 * n * V_ * d_);
     launches_++;
     if (arena) {

@@ -74,6 +74,51 @@ struct EpiParams {
   int H, Hkv, hd;
 };
 
+// ---- persistent decode-layer chain (decode_chain.cu) -------------------------
+// One launch runs a program of ops separated by grid barriers: weight GEMMs
+// (partials per stream-K segment into ws) and the reductions consuming them.
+enum ChainKind {
+  kChGemm = 0,   // X[T, K] . W[N, K]^T (X = TMA map xmap: 0 a, 1 o, 2 h), reduced per tile with `red`
+  kChPrep = 1,   // out = bf16(x * g); ssq[t][tile] (the input side of an RMSNorm)
+};
+enum ChainRed {
+  kRedResid = 0,    // x += W.X (+ xpeer store); if g: out = bf16(x * g), ssq[t][tile]
+  kRedSwiGLU = 1,   // out[t][j] = bf16(silu(inv_t (W.X)[2j]) * inv_t (W.X)[2j+1])
+  kRedQKV = 2,      // ep (RoPE + q store + paged K/V write) of inv_t * W.X
+};
+constexpr int kChainMaxOps = 12;
+constexpr int kChainSsqStride = 128;   // ssq[tile][token] row stride (T <= 128; d / 128 <= 128 tiles)
+constexpr int kChainMaxTiles = 512;    // 128-row weight tiles per GEMM op
+struct ChainOp {
+  int kind, red;
+  const bf16* w;     // kChGemm: tile-packed weights [N (padded to 128), K]
+  int N, K, xmap;
+  float* x;          // kRedResid / kChPrep: fp32 residual [T, d]
+  float* xpeer;      // kRedResid: also store the updated rows here (stage hand-off; nullable)
+  const bf16* g;     // kRedResid / kChPrep: the next RMSNorm's gain (nullptr: none)
+  bf16* out;         // bf16(x * g) [T, d] (kRedResid, kChPrep); h [T, N/2] (kRedSwiGLU)
+  EpiParams ep;      // kRedQKV
+};
+struct ChainProgram {
+  ChainOp op[kChainMaxOps];
+  int n_ops;
+  int T, d;
+  float eps;
+  float* ws;                  // segment partials [(tiles + grid) * T * 128] fp32 (largest GEMM)
+  float* ssq;                 // [d / 128][kChainSsqStride] per-tile sums of squares of x
+  int* cnt;                   // [2][kChainMaxTiles] zero-initialised tile arrival counters (re-armed by the kernel)
+  int cnt_parity;             // buffer of this launch's first GEMM op (the host alternates, chain_gemms)
+  unsigned long long* bar;    // grid-barrier counter (monotone over the engine's lifetime)
+  unsigned long long bar_base;   // its value when this launch starts
+  int trace_on;               // TDP_CHAIN_TRACE builds: stamp this launch (decode_chain.cu)
+};
+// grid = number of SMs (one CTA each); T <= 128; maps = X operands a / o / h
+// described with box rows 32 (T <= 32), 64 (T <= 64) or 128.  The counter
+// advances by grid * chain_barriers(p).
+void launch_decode_chain(const ChainProgram& p, const CUtensorMap* maps, int grid, cudaStream_t st);
+int chain_barriers(const ChainProgram& p);
+int chain_gemms(const ChainProgram& p);   // GEMM ops: the counter parity advances by this much
+
 // ---- attention --------------------------------------------------------------
 // Decode: one query token per sequence; q [n, H*hd] (physical RoPE-pair order),
 // paged K/V via block tables; o [n, H*hd] bf16.  Split-KV over split_tokens

@@ -10,8 +10,100 @@
 
 using namespace tdp;
 
+// Device buffers of a decode-chain test program (testing only).
+struct ChainBufs {
+  float *ws = nullptr, *ssq = nullptr;
+  int* cnt = nullptr;
+  unsigned long long* bar = nullptr;
+  int nsm = 0;
+  bool alloc(int device, int max_tiles) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&ws, (size_t)(max_tiles + nsm) * 128 * 128 * 4) || cudaMalloc(&ssq, 128 * kChainSsqStride * 4) ||
+        cudaMalloc(&cnt, 1024 * 4) || cudaMalloc(&bar, 8))
+      return false;
+    cudaMemset(cnt, 0, 1024 * 4);
+    cudaMemset(bar, 0, 8);
+    return true;
+  }
+  void fill(ChainProgram& P, int T, int d) const {
+    P.T = T;
+    P.d = d;
+    P.eps = 1e-5f;
+    P.ws = ws;
+    P.ssq = ssq;
+    P.cnt = cnt;
+    P.bar = bar;
+    P.bar_base = 0;
+  }
+  ~ChainBufs() {
+    cudaFree(ws);
+    cudaFree(ssq);
+    cudaFree(cnt);
+    cudaFree(bar);
+  }
+};
+
+static bf16* upload_packed(const uint16_t* W, int N, int K) {
+  const int Np = (N + 127) / 128 * 128;
+  std::vector<uint16_t> pk((size_t)Np * K, 0);
+  for (int r = 0; r < N; ++r)
+    for (int c = 0; c < K; ++c) pk[pack_offset(r, c, K)] = W[(size_t)r * K + c];
+  bf16* d = nullptr;
+  if (cudaMalloc(&d, pk.size() * 2) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, pk.data(), pk.size() * 2, cudaMemcpyHostToDevice);
+  return d;
+}
+
+// The decode chain (decode_chain.cu) on one GEMM op with the residual tile
+// reduction into a zeroed residual: out[T, N] = X[T, K] . W[N, K]^T
+// (N % 128 == 0, T <= 128).  Testing only.
+static td_status test_chain_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N,
+                                 int32_t K, float* out) {
+  if (!A || !W || !out || T < 1 || T > 128 || N < 128 || N % 128 || K < 64 || K % 64) return TD_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
+  ChainBufs B;
+  bf16 *dA = nullptr, *dP = upload_packed(W, N, K);
+  float* x = nullptr;
+  td_status st = TD_OK;
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  if (!dP || !B.alloc(device, N / 128) || cudaMalloc(&dA, (size_t)128 * K * 2) || cudaMalloc(&x, (size_t)T * N * 4)) {
+    st = TD_ENOMEM;
+  } else {
+    cudaMemset(dA, 0, (size_t)128 * K * 2);
+    cudaMemcpy(dA, A, (size_t)T * K * 2, cudaMemcpyHostToDevice);
+    cudaMemset(x, 0, (size_t)T * N * 4);
+    TcOperand xo;
+    if (!make_tc_operand(&xo, dA, 128, K, T <= 32 ? 32 : T <= 64 ? 64 : 128)) {
+      st = TD_ECUDA;
+    } else {
+      ChainProgram P{};
+      P.op[0].kind = kChGemm;
+      P.op[0].red = kRedResid;
+      P.op[0].w = dP;
+      P.op[0].N = N;
+      P.op[0].K = K;
+      P.op[0].xmap = 0;
+      P.op[0].x = x;
+      P.n_ops = 1;
+      B.fill(P, T, N);
+      const CUtensorMap maps[3] = {xo.map, xo.map, xo.map};
+      launch_decode_chain(P, maps, B.nsm, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
+      if (take_launch_error() != cudaSuccess) st = TD_ECUDA;
+      if (st == TD_OK) cudaMemcpy(out, x, (size_t)T * N * 4, cudaMemcpyDeviceToHost);
+    }
+  }
+  cudaFree(dA);
+  cudaFree(dP);
+  cudaFree(x);
+  cudaStreamDestroy(s);
+  return st;
+}
+
 extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint16_t* W, int32_t T, int32_t N,
                                   int32_t K, int32_t impl, int32_t splits, float* out) {
+  if (impl == 5) return test_chain_gemm(device, A, W, T, N, K, out);
   if (!A || !W || !out || T < 1 || N < 2 || (N & 1) || K < 64 || K % 64) return TD_EINVAL;
   if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
   bf16 *dA = nullptr, *dW = nullptr;
@@ -230,3 +322,84 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
   cudaStreamDestroy(s);
   return st;
 }
+
+// The decode chain on an MLP block (testing only), with its split RMSNorm:
+//   a = bf16(x0 * g);  r_t = 1/rms(x0_t);
+//   h = bf16(silu(r_t Wgu[2j] . a) * (r_t Wgu[2j+1] . a));  x = x0 + Wd . h
+// ops: prep | gate/up GEMM (SwiGLU reduction) | down GEMM (residual reduction).
+extern "C" td_status td_test_chain_mlp(int32_t device, const float* x0, const uint16_t* g, const uint16_t* Wgu,
+                                       const uint16_t* Wd, int32_t T, int32_t d, int32_t F, float eps, uint16_t* a_out,
+                                       uint16_t* h_out, float* x_out) {
+  if (!x0 || !g || !Wgu || !Wd || !a_out || !h_out || !x_out || T < 1 || T > 128 || d < 128 || d % 128 || F < 64 ||
+      F % 64)
+    return TD_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TD_ECUDA;
+  ChainBufs B;
+  bf16 *dgu = upload_packed(Wgu, 2 * F, d), *dd = upload_packed(Wd, d, F);
+  bf16 *da = nullptr, *dh = nullptr, *dg = nullptr;
+  float* x = nullptr;
+  td_status st = TD_OK;
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  if (!dgu || !dd || !B.alloc(device, (2 * F + 127) / 128) || cudaMalloc(&da, (size_t)128 * d * 2) ||
+      cudaMalloc(&dh, (size_t)128 * F * 2) || cudaMalloc(&dg, (size_t)d * 2) || cudaMalloc(&x, (size_t)T * d * 4)) {
+    st = TD_ENOMEM;
+  } else {
+    cudaMemset(da, 0, (size_t)128 * d * 2);
+    cudaMemset(dh, 0, (size_t)128 * F * 2);
+    cudaMemcpy(dg, g, (size_t)d * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(x, x0, (size_t)T * d * 4, cudaMemcpyHostToDevice);
+    const int box = T <= 32 ? 32 : T <= 64 ? 64 : 128;
+    TcOperand xa, xh;
+    if (!make_tc_operand(&xa, da, 128, d, box) || !make_tc_operand(&xh, dh, 128, F, box)) {
+      st = TD_ECUDA;
+    } else {
+      ChainProgram P{};
+      int n = 0;
+      P.op[n].kind = kChPrep;
+      P.op[n].x = x;
+      P.op[n].g = dg;
+      P.op[n++].out = da;
+      P.op[n].kind = kChGemm;
+      P.op[n].red = kRedSwiGLU;
+      P.op[n].w = dgu;
+      P.op[n].N = 2 * F;
+      P.op[n].K = d;
+      P.op[n].xmap = 0;
+      P.op[n++].out = dh;
+      P.op[n].kind = kChGemm;
+      P.op[n].red = kRedResid;
+      P.op[n].w = dd;
+      P.op[n].N = d;
+      P.op[n].K = F;
+      P.op[n].xmap = 2;
+      P.op[n++].x = x;
+      P.n_ops = n;
+      B.fill(P, T, d);
+      P.eps = eps;
+      const CUtensorMap maps[3] = {xa.map, xa.map, xh.map};
+      launch_decode_chain(P, maps, B.nsm, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) st = TD_ECUDA;
+      if (take_launch_error() != cudaSuccess) st = TD_ECUDA;
+      if (st == TD_OK) {
+        cudaMemcpy(a_out, da, (size_t)T * d * 2, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h_out, dh, (size_t)T * F * 2, cudaMemcpyDeviceToHost);
+        cudaMemcpy(x_out, x, (size_t)T * d * 4, cudaMemcpyDeviceToHost);
+      }
+    }
+  }
+  cudaFree(da);
+  cudaFree(dh);
+  cudaFree(dg);
+  cudaFree(dgu);
+  cudaFree(dd);
+  cudaFree(x);
+  cudaStreamDestroy(s);
+  return st;
+}
+
+#ifdef TDP_CHAIN_TRACE
+namespace tdp { void chain_trace_read(unsigned long long* out); }
+// measurement builds only: the decode chain's trace buffer (see decode_chain.cu)
+extern "C" void td_chain_trace(unsigned long long* out) { tdp::chain_trace_read(out); }
+#endif

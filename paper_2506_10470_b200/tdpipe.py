@@ -42,7 +42,8 @@ class td_options(C.Structure):
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_ids", C.c_void_p),
                 ("p2d_kv_permille", C.c_int32), ("d2p_finish_permille", C.c_int32), ("hb_tokens", C.c_int32),
                 ("handoff", C.c_int32), ("allgather", ALLGATHER_FN), ("allgather_user", C.c_void_p),
-                ("hbm_peak_gbs", C.c_double), ("tc_peak_tflops", C.c_double)]
+                ("hbm_peak_gbs", C.c_double), ("tc_peak_tflops", C.c_double),
+                ("decode_chain", C.c_int32)]
 
 
 class td_run_stats(C.Structure):
@@ -70,7 +71,7 @@ class td_batch(C.Structure):
 EXPORTS = ["td_default_options", "td_create", "td_destroy", "td_last_error", "td_submit", "td_upload",
            "td_run", "td_get_output", "td_get_outputs", "td_get_logits", "td_reset", "td_stage_forward",
            "td_kv_reset", "td_profile", "td_load_profile", "td_get_log", "td_info", "td_set_timing",
-           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace",
+           "td_get_timing", "td_nccl_ids", "td_test_gemm", "td_test_chain_mlp", "td_bench_gemm", "td_bench_attn", "td_simulate", "td_write_trace",
            "td_get_weight", "td_bench_step", "td_get_launch_bytes"]
 
 
@@ -114,6 +115,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.td_write_trace.argtypes = [C.c_void_p, C.c_char_p]
     lib.td_test_gemm.argtypes = [C.c_int32, P(C.c_uint16), P(C.c_uint16), C.c_int32, C.c_int32, C.c_int32,
                                  C.c_int32, C.c_int32, P(C.c_float)]
+    lib.td_test_chain_mlp.argtypes = [C.c_int32, P(C.c_float), P(C.c_uint16), P(C.c_uint16), P(C.c_uint16),
+                                      C.c_int32, C.c_int32, C.c_int32, C.c_float, P(C.c_uint16), P(C.c_uint16),
+                                      P(C.c_float)]
     for f in EXPORTS:
         if f not in ("td_default_options", "td_destroy", "td_last_error", "td_submit"):
             getattr(lib, f).restype = C.c_int32
@@ -380,3 +384,24 @@ def td_bench_attn(ctx, H: int, Hkv: int, hd: int, iters: int = 50, device: int =
     if st != TD_OK:
         raise TDError(f"td_bench_attn failed: {st}")
     return us.value
+
+
+def td_test_chain_mlp(x0: np.ndarray, g_bits: np.ndarray, Wgu_bits: np.ndarray, Wd_bits: np.ndarray,
+                      eps: float = 1e-5, device: int = 0):
+    """Kernel unit test of the decode chain on one MLP block: returns
+    (a bf16 bits [T, d], h bf16 bits [T, F], x fp32 [T, d])."""
+    x0 = np.ascontiguousarray(x0, dtype=np.float32)
+    g = np.ascontiguousarray(g_bits, dtype=np.uint16)
+    Wgu = np.ascontiguousarray(Wgu_bits, dtype=np.uint16)
+    Wd = np.ascontiguousarray(Wd_bits, dtype=np.uint16)
+    T, d = x0.shape
+    F = Wd.shape[1]
+    a = np.zeros((T, d), np.uint16)
+    h = np.zeros((T, F), np.uint16)
+    x = np.zeros((T, d), np.float32)
+    st = lib().td_test_chain_mlp(device, _ptr(x0, C.c_float), _ptr(g, C.c_uint16), _ptr(Wgu, C.c_uint16),
+                                 _ptr(Wd, C.c_uint16), T, d, F, eps, _ptr(a, C.c_uint16), _ptr(h, C.c_uint16),
+                                 _ptr(x, C.c_float))
+    if st != TD_OK:
+        raise TDError(f"td_test_chain_mlp failed: {st}")
+    return a, h, x

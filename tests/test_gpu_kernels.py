@@ -49,3 +49,57 @@ def test_gemm_token_major_split_k_vs_fp64(T, N, K, splits):
     err = np.abs(out - ref).max() / max(np.abs(ref).max(), 1e-6)
     assert err < 2e-5, err
     assert np.array_equal(td_test_gemm(Ab, Wb, impl=4, splits=splits), out)
+
+
+@pytest.mark.parametrize("T,N,K", [(1, 128, 64), (4, 256, 64), (7, 256, 256), (32, 4096, 4096), (8, 4096, 11008),
+                                   (33, 1024, 1024), (64, 8192, 1024), (100, 512, 4096), (128, 22016, 4096)])
+def test_chain_gemm_vs_fp64(T, N, K):
+    """The persistent decode chain (impl 5): a GEMM op split stream-K style into
+    (CTA, weight tile) segments, each tile reduced in CTA order by the CTA that
+    completes it (ticket) into a zeroed residual --
+    the engine's path for decode micro-batches of <= 128 tokens; bitwise
+    repeatable."""
+    rng = np.random.default_rng(T * 11 + N + K)
+    Ab, Af = _bf16(rng, (T, K))
+    Wb, Wf = _bf16(rng, (N, K), 1.0 / np.sqrt(K))
+    out = td_test_gemm(Ab, Wb, impl=5)
+    ref = Af @ Wf.T
+    err = np.abs(out - ref).max() / max(np.abs(ref).max(), 1e-6)
+    assert err < 2e-5, err
+    assert np.array_equal(td_test_gemm(Ab, Wb, impl=5), out)
+
+
+def _bits_to_f64(b):
+    return torch.from_numpy(b.view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+
+
+@pytest.mark.parametrize("T,d,F", [(1, 128, 256), (4, 256, 512), (9, 1024, 2816), (40, 512, 1536), (128, 1024, 1024)])
+def test_chain_mlp_vs_fp64(T, d, F):
+    """Decode chain on one MLP block with its split RMSNorm (prep: a = bf16(x0*g)
+    and sums of squares | gate/up GEMM, tile reductions scale by 1/rms and apply
+    SwiGLU | down GEMM, tile reductions add into the residual; grid barriers
+    between) vs the plain definition in fp64.  a and h are checked to 1 bf16
+    ulp; the residual is recomputed from the kernel's own h, so its fp32
+    tolerance is tight."""
+    from paper_2506_10470_b200.tdpipe import td_test_chain_mlp
+    rng = np.random.default_rng(T + d + F)
+    x0 = rng.standard_normal((T, d)).astype(np.float32)
+    gb, gf = _bf16(rng, (d,), 0.5)
+    gb = gb.copy()
+    Wgub, Wguf = _bf16(rng, (2 * F, d), 1.0 / np.sqrt(d))
+    Wdb, Wdf = _bf16(rng, (d, F), 1.0 / np.sqrt(F))
+    a, h, x = td_test_chain_mlp(x0, gb, Wgub, Wdb)
+    xr = x0.astype(np.float64)
+    a_k = _bits_to_f64(a)
+    a_ref = xr * gf
+    assert np.abs(a_k - a_ref).max() <= 2 ** -8 * np.abs(a_ref).max()
+    inv = 1.0 / np.sqrt((xr * xr).mean(axis=1, keepdims=True) + 1e-5)
+    gu = (a_k @ Wguf.T) * inv
+    g_, u_ = gu[:, 0::2], gu[:, 1::2]
+    h_ref = g_ / (1 + np.exp(-g_)) * u_
+    h_k = _bits_to_f64(h)
+    assert np.abs(h_k - h_ref).max() <= 2 ** -7 * np.abs(h_ref).max() + 1e-6
+    x_ref = xr + h_k @ Wdf.T
+    assert np.abs(x - x_ref).max() <= 2e-5 * np.abs(x_ref).max()
+    a2, h2, x2 = td_test_chain_mlp(x0, gb, Wgub, Wdb)
+    assert np.array_equal(x2, x) and np.array_equal(a2, a) and np.array_equal(h2, h)

@@ -304,12 +304,14 @@ def test_llama7b_shaped_bench_launch_config():
 
 
 @pytest.mark.slow
-def test_llama7b_split_k_decode_tolerance():
+@pytest.mark.parametrize("chain", [0, 1], ids=["per_kernel", "decode_chain"])
+def test_llama7b_split_k_decode_tolerance(chain):
     """Decode micro-batches of 1, 8 and 40 sequences at Llama-2-7B width, where
     the decode GEMMs split K (8 / 8 / 4 splits on QKV, O, gate-up, down) and
     attention splits the context: every sequence's logits vs the fp64 oracle,
     and the same sequence decoded in different batch compositions agrees
-    within the tolerance (split counts change rounding, never the result)."""
+    within the tolerance (split counts change rounding, never the result).
+    decode_chain: the same through the persistent decode-layer kernel."""
     shape = SHAPES["llama2_7b"].with_layers(2)
     wl = generate_workload(48, shape.vocab, 21)
     prompts = [r.prompt for r in wl.requests][:40]
@@ -317,7 +319,7 @@ def test_llama7b_split_k_decode_tolerance():
     W = OracleWeights(shape)
     res = {}
     for b in (1, 8, 40):
-        t = TDPipe(shape, 1, kv_blocks=4096)
+        t = TDPipe(shape, 1, kv_blocks=4096, decode_chain=chain)
         bt = _paged([L + 2 for L in lengths[:b]])
         out = _prefill_in_budget(t, prompts[:b], bt)
         nxt = np.argmax(out, -1).astype(np.int32)
@@ -532,3 +534,52 @@ def test_td_run_trace_and_kv_timeline(tmp_path):
     kv_sim = [e["args"]["blocks"] for e in json.load(open(path2))["traceEvents"] if e["ph"] == "C"]
     assert kv == kv_sim
     assert max(kv) <= C
+
+
+@pytest.mark.parametrize("shape", [GQA8, GQA4_64], ids=lambda s: s.name)
+def test_decode_chain_stage_forward(shape):
+    """The persistent decode-layer kernel (td_options.decode_chain = 1): a
+    ragged prefill, then 3 decode steps; logits vs the fp64 oracle, and equal
+    within the tolerance to the per-kernel path on the same inputs."""
+    W = OracleWeights(shape)
+    rng = np.random.default_rng(5)
+    lengths = [1, 17, 300, 5, 64]
+    prompts = [rng.integers(0, shape.vocab, size=L).astype(np.int32) for L in lengths]
+    bt = _paged([L + 4 for L in lengths])
+    outs = {}
+    for chain in (0, 1):
+        t = TDPipe(shape, 1, kv_blocks=512, decode_chain=chain)
+        out = t.td_stage_forward(0, TD_BATCH_PREFILL, [0] * 5, lengths, bt, np.concatenate(prompts))
+        seqs = [list(p) for p in prompts]
+        steps = []
+        for step in range(3):
+            nxt = [int(np.argmax(o)) for o in out] if chain == 0 else outs[0][step][0]
+            for i in range(5):
+                seqs[i].append(nxt[i])
+            out = t.td_stage_forward(0, TD_BATCH_DECODE, [len(s) - 1 for s in seqs], [1] * 5, bt,
+                                     np.array(nxt, np.int32))
+            steps.append((nxt, out, [list(s_) for s_ in seqs]))
+        t.close()
+        outs[chain] = steps
+    for (nxt0, out0, seqs0), (nxt1, out1, _) in zip(outs[0], outs[1]):
+        for i in range(5):
+            ref = F.sequence_logits(W, np.array(seqs0[i]))[-1]
+            _rows_ok(out1[i], ref)
+            assert F.max_abs_rel(out1[i], out0[i]).max() <= TOL
+
+
+def test_decode_chain_td_run_teacher_forced(tmp_path):
+    """td_run end to end (2 stages, prefill + decode phases) with the decode
+    chain: teacher-forced logits vs the oracle, decisions bit-exact."""
+    shape = GQA4_64
+    wl = generate_workload(12, shape.vocab, 3, uniform_in=(4, 60), uniform_out=(4, 24))
+    csv = str(tmp_path / "p.csv")
+    write_profile_csv(csv, *synthetic_profile(64, 2048))
+    st, toks, logits, log = _tiny_run(shape, wl, 2, csv, kv_blocks=256, decode_chain=1)
+    W = OracleWeights(shape)
+    for r, tk, lg in zip(wl.requests, toks, logits):
+        assert len(tk) == r.max_new_tokens
+        _rows_ok(lg, F.teacher_forced_logits(W, r.prompt, tk))
+    reqs = [(len(r.prompt), r.predicted_len, r.max_new_tokens) for r in wl.requests]
+    ref = schedule(reqs, SchedOptions(n_stages=2, block_size=16, kv_blocks=256), *synthetic_profile(64, 2048))
+    assert log == "".join(l + "\n" for l in ref.log)
