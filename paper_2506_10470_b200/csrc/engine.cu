@@ -281,7 +281,6 @@ class CudaEngine : public Engine {
 };
 
 enum Cls { cDecAttn = 0, cPreAttn, cQKV, cO, cGU, cDown, cLM, cNorm, cStage, cMB };
-constexpr int kSkTicketOff = 1 << 15;   // counters_[kSkTicketOff ..]: stream-K GEMM tile tickets
 constexpr int kDecOff = 8;   // decode-phase GEMM classes = prefill class + kDecOff
 constexpr int kAttnBucket = 15, kGemmBucket = 19;
 constexpr int cChain = 23;   // the persistent decode-layer chain (T <= 128)   // + bucket(n): batch-size buckets for decode

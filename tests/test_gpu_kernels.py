@@ -103,3 +103,4 @@ def test_chain_mlp_vs_fp64(T, d, F):
     assert np.abs(x - x_ref).max() <= 2e-5 * np.abs(x_ref).max()
     a2, h2, x2 = td_test_chain_mlp(x0, gb, Wgub, Wdb)
     assert np.array_equal(x2, x) and np.array_equal(a2, a) and np.array_equal(h2, h)
+
