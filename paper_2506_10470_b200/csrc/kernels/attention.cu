@@ -1048,9 +1048,11 @@ void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st) {
 // ------------------------------------------------------------------ prefill
 // Varlen causal flash attention on tensor cores (mma.sync m16n8k16 bf16, fp32
 // softmax), K/V read from the paged cache the QKV epilogue just wrote.  Grid:
-// (64-query tile, sequence, head); 4 warps x 16 query rows; 64-key tiles
-// double-buffered with cp.async; S = Q K^T and O += P V with P kept in
-// registers (accumulator layout == A-fragment layout).  Prefill is < 1% of the
+// (sequence, head, 64-query tile from the sequence's end: longest causal
+// ranges first); 4 warps x 16 query rows; 64-key tiles double-buffered with
+// cp.async, the Q tile staged in K stage 1 (64 KB smem: 3 CTAs / SM); S = Q K^T
+// and O += P V with P kept in registers (accumulator layout == A-fragment
+// layout).  Prefill is < 1% of the
 // prefill FLOPs at ShareGPT lengths, so mma.sync suffices.
 namespace {
 TDP_DEV void ldsm_x4(uint32_t* r, uint32_t addr) {
@@ -1079,22 +1081,30 @@ TDP_DEV int fswz(int r, int c) {   // 16-byte chunk index inside a [64][HD] bf16
 }
 }  // namespace
 
+#ifndef TDP_PREFILL_MINB
+#define TDP_PREFILL_MINB 3
+#endif
 template <int HD>
-__global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p) {
+__global__ void __launch_bounds__(128, HD >= 128 ? TDP_PREFILL_MINB : 4) flash_prefill_kernel(PrefillAttnParams p) {
   constexpr int BQ = 64, BKV = 64, CH = HD / 8;
   constexpr int TILE = BQ * HD * 2;
   extern __shared__ __align__(128) uint8_t fsm[];
-  uint8_t* sQ = fsm;
-  uint8_t* sK = fsm + TILE;          // 2 stages
-  uint8_t* sV = fsm + 3 * TILE;      // 2 stages
+  uint8_t* sK = fsm;                 // 2 stages
+  uint8_t* sV = fsm + 2 * TILE;      // 2 stages
+  uint8_t* sQ = sK + TILE;           // aliases K stage 1: Q goes to registers before tile 1 is loaded
   pdl_trigger_tail(2);
   pdl_wait();
-  const int qt = blockIdx.x, seq = blockIdx.y, h = blockIdx.z;
+  // grid (sequence, head, query tile counted from the END of the sequence):
+  // the tiles with the most causal key tiles of every (sequence, head) are in
+  // the first blocks launched, the short ones fill the tail
+  const int seq = blockIdx.x, h = blockIdx.y;
   const int L = p.seq_ctx[seq];                  // keys: positions 0 .. L-1
   const int qs = p.seq_qstart ? p.seq_qstart[seq] : 0;
   const int nq = L - qs;                         // queries: positions qs .. L-1
+  const int n_qt = (nq + BQ - 1) / BQ;
+  if ((int)blockIdx.z >= n_qt) return;
+  const int qt = n_qt - 1 - (int)blockIdx.z;
   const int q0 = qt * BQ;                        // (query indices relative to qs)
-  if (q0 >= nq) return;
   const int row0 = p.seq_last[seq] - nq + 1;    // token row of query 0
   const int G = p.H / p.Hkv, kh = h / G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1134,14 +1144,20 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
   const int qr0 = q0 + warp * 16 + g;     // this thread's two queries (relative): qr0, qr0 + 8
 
   for (int kt = 0; kt < n_kt; ++kt) {
-    if (kt + 1 < n_kt) load_kv((kt + 1) & 1, (kt + 1) * BKV);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (kt == 0) {
+    if (kt == 0) {   // Q and K/V tile 0 landed; Q to registers, then its buffer becomes stage 1
+      cp_async_wait<0>();
+      __syncthreads();
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk)
         ldsm_x4(qf[kk], smem_u32(sQ + fswz<HD>(warp * 16 + (lane & 15), kk * 2 + (lane >> 4)) * 16));
+      __syncthreads();
+      if (n_kt > 1) load_kv(1, BKV);
+      cp_async_commit();
+    } else {
+      if (kt + 1 < n_kt) load_kv((kt + 1) & 1, (kt + 1) * BKV);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
     }
     const uint8_t* K = sK + (kt & 1) * TILE;
     const uint8_t* V = sV + (kt & 1) * TILE;
@@ -1238,13 +1254,13 @@ __global__ void __launch_bounds__(128) flash_prefill_kernel(PrefillAttnParams p)
 
 template <int HD>
 static void launch_flash(const PrefillAttnParams& p, cudaStream_t st) {
-  constexpr int smem = 5 * 64 * HD * 2;
+  constexpr int smem = 4 * 64 * HD * 2;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(flash_prefill_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  dim3 grid((p.max_len + 63) / 64, p.n_seqs, p.H);
+  dim3 grid(p.n_seqs, p.H, (p.max_len + 63) / 64);
   launch_k(flash_prefill_kernel<HD>, grid, dim3(128), smem, st, p);
 }
 
