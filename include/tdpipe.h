@@ -330,8 +330,9 @@ td_status td_test_chain_mlp(int32_t device, const float* x0, const uint16_t* g, 
  * the tcgen05 GEMM on [T, K] x [N, K]^T (tile-packed weights, fp32 output),
  * cycling over `copies` weight buffers so that the weights stream from HBM;
  * splits = split-K count (1 = none); decode = 1 selects the swap-AB decode
- * kernel (weight rows x token tiles), decode = 2 the token-major kernel with
- * `splits` K splits (reduction + epilogue launch included). */
+ * kernel (weight rows x token tiles; 3 / 4: with 64- / 32-token tiles),
+ * decode = 2 the token-major kernel with `splits` K splits (reduction +
+ * epilogue launch included). */
 td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t splits, int32_t decode,
                         int32_t iters, int32_t copies, float* us_per_call);
 

@@ -618,9 +618,12 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
              (int64_t)(splits + 1) * T * ((N + 127) / 128 * 128) <= ws_cap_)
         ++splits;
     }
-  } else if (decode) {
+  }
+  if (decode) {
     // split-K to ~288 CTAs (about 2 per SM), at most 8 splits, >= 4 k-blocks
-    // per split, partials within the workspace (scripts/gemm_sweep.py)
+    // per split, partials within the workspace (scripts/gemm_sweep.py).
+    // (Half-width token tiles at 33..128 tokens measured faster isolated but
+    // slower in the job: profiles/r2/ab/README.md.)
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
     splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, 288 / ctas));

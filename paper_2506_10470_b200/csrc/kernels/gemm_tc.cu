@@ -434,7 +434,7 @@ int effective_splits(int K, int splits) {
 }
 
 int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
-                   int* counters, bool decode, cudaStream_t st, bool defer_reduce) {
+                   int* counters, bool decode, cudaStream_t st, bool defer_reduce, int bn) {
   if (T <= 0) return 1;
   if (!decode && W.packed && T > 128) {
     // prefill / 129+-token decode: token-major tiles (vectorised epilogue),
@@ -461,7 +461,7 @@ int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const Epi
     }
     return nsplit;
   }
-  switch (tc_bn_for(T, decode)) {
+  switch (bn > 0 ? bn : tc_bn_for(T, decode)) {
     // <= 110 KB of smem for BN <= 128 so that two CTAs share an SM
     case 32: launch_bn<32, 5>(W, Xby_bn[0], T, ep, splits, ws, counters, defer_reduce, st); break;
     case 64: launch_bn<64, 4>(W, Xby_bn[1], T, ep, splits, ws, counters, defer_reduce, st); break;

@@ -25,8 +25,10 @@ int tc_bn_for(int T, bool decode);
 // [tiles][splits][128][BN] fp32 and zero-initialised per-tile counters.
 // Returns the split count actually used.  defer_reduce: leave the partials in
 // ws [splits][T][N] for a fused consumer (launch_resid_norm) instead of
-// launching the reduction + epilogue.
+// launching the reduction + epilogue.  bn > 0: the swap-AB token tile (32 /
+// 64 / 128 / 256) instead of tc_bn_for's (token tiles share each weight tile
+// through L2).
 int launch_gemm_tc(const TcOperand& W, const TcOperand* Xby_bn, int T, const EpiParams& ep, int splits, float* ws,
-                   int* counters, bool decode, cudaStream_t st, bool defer_reduce = false);
+                   int* counters, bool decode, cudaStream_t st, bool defer_reduce = false, int bn = 0);
 
 }  // namespace tdp

@@ -200,7 +200,9 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
       st = TD_ECUDA;
     } else {
       auto call = [&](int i) {
-        launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode == 1, s);   // 2: token-major (+ split-K)
+        // 1: swap-AB (3: with 64-token tiles, 4: 32-token tiles); 2: token-major (+ split-K)
+        launch_gemm_tc(w[i % copies], x, T, ep, splits, ws, cnt, decode == 1 || decode >= 3, s, false,
+                       decode == 3 ? 64 : decode == 4 ? 32 : 0);
       };
       for (int i = 0; i < 3; ++i) call(i);
       cudaEvent_t a, b;
