@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--ctx", type=int, default=600)
 ap.add_argument("--bmax", type=int, default=256)
-ap.add_argument("--chain", type=int, default=1)
+ap.add_argument("--chain", type=int, default=0)
 ap.add_argument("--model", default="llama2_7b")
 a = ap.parse_args()
 shape = SHAPES[a.model].with_layers(a.layers)
@@ -24,7 +24,7 @@ csv = os.path.join(tempfile.gettempdir(), f"step_ab_{os.getpid()}.csv")
 t.td_profile(csv, a.bmax, 2048, a.ctx)
 tdec, tpre = read_profile_csv(csv)
 row = {"tag": os.environ.get("TAG", ""), "model": a.model, "chain": a.chain, "layers": a.layers, "ctx": a.ctx}
-for b in (1, 4, 8, 16, 32, 64, 128, 256):
+for b in (1, 4, 8, 16, 32, 64, 128, 256, 384, 512):
     if b <= a.bmax:
         row[f"D{b}"] = round(int(tdec[b]) / 1e3, 1)
 for k in (512, 2048):
