@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)t * d);
   float4* xp = xpeer ? reinterpret_cast<float4*>(xpeer + (int64_t)t * d) : nullptr;
   __shared__ float red[4];
-  __shared__ float part_ss;
+  __shared__ float part_ss[RC];   // every rank's partial sum of squares, written by that rank
   float ss = 0.f;
   for (int j = j0 + threadIdx.x; j < j0 + per / 4; j += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -255,12 +255,15 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x == 0) part_ss = red[0] + red[1] + red[2] + red[3];
+  // broadcast this rank's partial into slot [rank] of every rank's array, then
+  // one cluster barrier: afterwards each rank reads only its own shared memory,
+  // so no second barrier has to keep the peers' memory alive
+  if (threadIdx.x < RC) *cl.map_shared_rank(&part_ss[rank], threadIdx.x) = red[0] + red[1] + red[2] + red[3];
   cl.sync();
   if (!g) return;
   float tot = 0.f;
-  for (int r = 0; r < RC; ++r) tot += *cl.map_shared_rank(&part_ss, r);   // fixed order: deterministic
-  cl.sync();                                   // peers keep their smem until everyone has read it
+#pragma unroll
+  for (int r = 0; r < RC; ++r) tot += part_ss[r];   // fixed order: deterministic
   const float inv = rsqrtf(tot / (float)d + eps);
   const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g);
   uint2* o = reinterpret_cast<uint2*>(out + (int64_t)t * d);
