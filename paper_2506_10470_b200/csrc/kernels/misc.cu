@@ -278,24 +278,32 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
   }
 }
 
+#ifndef TDP_RN_CLUSTER
+#define TDP_RN_CLUSTER 8
+#endif
+// CTAs per token row (small batches).  Per 8-layer decode step at b = 1 the
+// reductions cost 156 / 107 / 75 / 77 us of marginal time with 2 / 4 / 8 / 16
+// (profiles/r2/timeline/README.md)
+constexpr int kRnCluster = TDP_RN_CLUSTER;
+
 void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
                        cudaStream_t st, float* xpeer) {
   if (T <= 0) return;
-  if (T <= 64 && d % (8 * 4) == 0) {
+  if (T <= 64 && d % (kRnCluster * 4) == 0) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(8, T);
+    cfg.gridDim = dim3(kRnCluster, T);
     cfg.blockDim = dim3(128);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 8;
+    attr[0].val.clusterDim.x = kRnCluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    note_launch_error(cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<8>, ws, splits, x, g, out, T, d, eps, xpeer));
+    note_launch_error(cudaLaunchKernelEx(&cfg, resid_norm_cluster_kernel<kRnCluster>, ws, splits, x, g, out, T, d, eps, xpeer));
   } else {
     launch_k(resid_norm_kernel<256>, dim3(T), dim3(256), 0, st, ws, splits, x, g, out, T, d, eps, xpeer);
   }
