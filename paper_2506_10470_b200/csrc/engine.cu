@@ -790,13 +790,14 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
   const int T = M.T, n = M.n;
   const int nqkv = (H_ + 2 * Hkv_) * hd_;
   const float eps = s_.rms_eps;
-  if (stage == 0) {
-    launch_embed(arena, dm + M.o_tokidx, E_, x_, T, d_, st_);
-    launches_++;
-  }
-  if (stage == S_ - 1) launches_++;   // final norm
   const bool dec = !M.prefill;
-  bool normed = false;   // a_ already holds RMSNorm(x; g1) (fused into the previous down-proj reduction)
+  bool normed = false;   // a_ already holds RMSNorm(x; g1) (fused into the embedding / the previous down-proj reduction)
+  if (stage == 0) {   // + the first layer's input norm
+    launch_embed(arena, dm + M.o_tokidx, E_, x_, T, d_, st_, L_[stage_l0_[stage]].g1, a_, eps);
+    launches_++;
+    normed = true;
+  }
+  bool final_normed = false;   // decode at the last stage: the final norm rides on the last down-proj reduction
   for (int l = stage_l0_[stage]; l < stage_l1_[stage]; ++l) {
     const LayerW& w = L_[l];
     bf16* kvl = kv_ + (int64_t)(l - own_l0_) * C_ * (kv_block_bytes_layer_ / 2);
@@ -909,7 +910,11 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     tend(idn, (double)d_ * F_ * 2 + (double)T * F_ * 2 + 8.0 * T * d_, 2.0 * T * d_ * F_);
     if (sd > 1) {   // reduce + residual, fused with the next layer's input norm when it is in this stage
       const bool last_layer = l + 1 == stage_l1_[stage];
-      const bf16* gnext = !last_layer ? L_[l + 1].g1 : nullptr;
+      // decode micro-batches (one token per sequence: row i = sequence i) at
+      // the last stage also get the final norm here instead of a launch
+      const bool fin = last_layer && stage == S_ - 1 && dec && !M.hybrid;
+      const bf16* gnext = !last_layer ? L_[l + 1].g1 : fin ? gf_ : nullptr;
+      final_normed = fin;
       // the stage's final residual rows are also stored straight into the
       // next stage's receive slot (peer store over NVLink; no separate send)
       float* xp = last_layer ? xpeer : nullptr;
@@ -920,7 +925,10 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     }
   }
   if (stage == S_ - 1) {
-    launch_rmsnorm(x_, gf_, a_, dm + M.o_last, n, d_, eps, st_);
+    if (!final_normed) {
+      launch_rmsnorm(x_, gf_, a_, dm + M.o_last, n, d_, eps, st_);
+      launches_++;   // final norm
+    }
     EpiParams el{};
     el.mode = kEpiF32;
     el.out_f32 = logits_;

@@ -40,7 +40,8 @@ void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st);
 
 // ---- embedding / norms / sampling -----------------------------------------
 void launch_embed(const int32_t* arena, const int32_t* tok_idx, const bf16* E, float* x, int T, int d,
-                  cudaStream_t st);
+                  cudaStream_t st, const bf16* g = nullptr, bf16* out = nullptr, float eps = 0.f);
+// (with g: also out[t] = bf16(RMSNorm(x[t]) * g), the first layer's input norm)
 // out[i] = bf16(RMSNorm(x[rows ? rows[i] : i]) * g)
 void launch_rmsnorm(const float* x, const bf16* g, bf16* out, const int32_t* rows, int n, int d, float eps,
                     cudaStream_t st);

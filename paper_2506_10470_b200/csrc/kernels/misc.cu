@@ -89,26 +89,52 @@ void launch_init(bf16* dst, const InitSpec& s, uint64_t seed, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------- embedding
-__global__ void embed_kernel(const int32_t* __restrict__ arena, const int32_t* __restrict__ tok_idx,
-                             const bf16* __restrict__ E, float* __restrict__ x, int d) {
+// x[t] = E[token] (fp32 residual); with g: also out[t] = bf16(RMSNorm(x[t]) * g),
+// the first layer's input norm (one launch fewer per micro-batch)
+__global__ void __launch_bounds__(128) embed_kernel(const int32_t* __restrict__ arena,
+                                                    const int32_t* __restrict__ tok_idx, const bf16* __restrict__ E,
+                                                    float* __restrict__ x, int d, const bf16* __restrict__ g,
+                                                    bf16* __restrict__ out, float eps) {
   pdl_trigger_tail(8);
   pdl_wait();
   const int t = blockIdx.x;
   const int tok = arena[tok_idx[t]];
   const uint4* src = reinterpret_cast<const uint4*>(E + (int64_t)tok * d);
   float4* dst = reinterpret_cast<float4*>(x + (int64_t)t * d);
+  float ss = 0.f;
   for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
     float f[8];
     bf16x8_to_f32(src[i], f);
     dst[2 * i] = make_float4(f[0], f[1], f[2], f[3]);
     dst[2 * i + 1] = make_float4(f[4], f[5], f[6], f[7]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss += f[k] * f[k];
+  }
+  if (!g) return;
+  __shared__ float red[4];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  const float inv = rsqrtf((red[0] + red[1] + red[2] + red[3]) / (float)d + eps);
+  const uint4* gs = reinterpret_cast<const uint4*>(g);
+  uint4* o = reinterpret_cast<uint4*>(out + (int64_t)t * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    float f[8], gg[8];
+    bf16x8_to_f32(src[i], f);
+    bf16x8_to_f32(gs[i], gg);
+    uint4 pk;
+    pk.x = pack_bf16x2(f[0] * inv * gg[0], f[1] * inv * gg[1]);
+    pk.y = pack_bf16x2(f[2] * inv * gg[2], f[3] * inv * gg[3]);
+    pk.z = pack_bf16x2(f[4] * inv * gg[4], f[5] * inv * gg[5]);
+    pk.w = pack_bf16x2(f[6] * inv * gg[6], f[7] * inv * gg[7]);
+    o[i] = pk;
   }
 }
 
 void launch_embed(const int32_t* arena, const int32_t* tok_idx, const bf16* E, float* x, int T, int d,
-                  cudaStream_t st) {
+                  cudaStream_t st, const bf16* g, bf16* out, float eps) {
   if (T <= 0) return;
-  launch_k(embed_kernel, dim3(T), dim3(128), 0, st, arena, tok_idx, E, x, d);
+  launch_k(embed_kernel, dim3(T), dim3(128), 0, st, arena, tok_idx, E, x, d, g, out, eps);
 }
 
 // ------------------------------------------------------------------- RMSNorm
