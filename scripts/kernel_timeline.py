@@ -31,6 +31,7 @@ ap.add_argument("--model", default="llama2_7b")
 ap.add_argument("--chain", type=int, default=0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--trace", default="")
+ap.add_argument("--roles", type=int, default=1, help="label the GEMMs QKV / O / gate-up / down / LM head")
 a = ap.parse_args()
 torch.cuda.init()
 shape = SHAPES[a.model].with_layers(a.layers)
@@ -70,10 +71,16 @@ for b in a.b:
     steps = [ev[starts[k]:(starts[k + 1] if k + 1 < len(starts) else len(ev))] for k in range(len(starts))]
     marg, dur, cnt = collections.defaultdict(float), collections.defaultdict(float), collections.Counter()
     spans = []
+    roles = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down"]
     for st in steps:
         prev = st[0].time_range.start
+        ng = sum(1 for e in st if short(e.name).startswith("gemm"))
+        gi = 0
         for e in st:
             k = short(e.name)
+            if k.startswith("gemm") and a.roles:   # label: 4 per layer, the last one is the LM head
+                k = "gemm_lm_head" if gi == ng - 1 else roles[gi % 4]
+                gi += 1
             marg[k] += max(0, e.time_range.end - prev)
             dur[k] += e.time_range.end - e.time_range.start
             cnt[k] += 1
