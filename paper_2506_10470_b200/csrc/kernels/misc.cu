@@ -239,10 +239,10 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(const float* __restrict_
   }
 }
 
-// Small decode batches: a row is split over a cluster of RC CTAs (RC*128
-// threads); each reduces its slice of the split-K partials, and the row's sum
-// of squares is all-reduced through distributed shared memory, so the whole
-// GPU -- not T SMs -- streams the partials.
+// Decode batches of <= kRnClusterMaxT tokens: a row is split over a cluster of
+// RC CTAs (RC*128 threads); each reduces its slice of the split-K partials, and
+// the row's sum of squares is all-reduced through distributed shared memory, so
+// the whole GPU -- not T SMs -- streams the partials.
 template <int RC>
 __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __restrict__ ws, int splits,
                                                                   float* __restrict__ x, const bf16* __restrict__ g,
@@ -311,11 +311,19 @@ __global__ void __launch_bounds__(128) resid_norm_cluster_kernel(const float* __
 // reductions cost 156 / 107 / 75 / 77 us of marginal time with 2 / 4 / 8 / 16
 // (profiles/r2/timeline/README.md)
 constexpr int kRnCluster = TDP_RN_CLUSTER;
+#ifndef TDP_RN_CLUSTER_MAXT
+#define TDP_RN_CLUSTER_MAXT 512
+#endif
+// token rows up to which the cluster kernel is used (one CTA per row beyond):
+// at 128 / 256 tokens it cuts the reductions' marginal time per 8-layer step
+// 211 -> 143 / 167 -> 152 us and the step 3,257 -> 3,059 / 5,638 -> 5,199 us
+// (profiles/r2/timeline/README.md)
+constexpr int kRnClusterMaxT = TDP_RN_CLUSTER_MAXT;
 
 void launch_resid_norm(const float* ws, int splits, float* x, const bf16* g, bf16* out, int T, int d, float eps,
                        cudaStream_t st, float* xpeer) {
   if (T <= 0) return;
-  if (T <= 64 && d % (kRnCluster * 4) == 0) {
+  if (T <= kRnClusterMaxT && d % (kRnCluster * 4) == 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kRnCluster, T);
     cfg.blockDim = dim3(128);
