@@ -626,11 +626,8 @@ int CudaEngine::gemm(const XOps& xo, const TcOperand& W, int T, int N, int K, co
     // slower in the job: profiles/r2/ab/README.md.)
     const int bn = tc_bn_for(T, true);
     const int64_t ctas = (int64_t)((N + 127) / 128) * ((T + bn - 1) / bn);
-#ifndef TDP_RESID_MAX_SPLITS
-#define TDP_RESID_MAX_SPLITS 8
-#endif
-    const int64_t cap = ep.mode == kEpiResid ? TDP_RESID_MAX_SPLITS : 8;   // (A/B builds only)
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(cap, 288 / ctas));
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, 288 / ctas));   // (4 / 6 for O, down: slower,
+                                                                             //  profiles/r2/timeline/)
     while (splits > 1 && (K / 64) / splits < 4) --splits;
     while (splits > 1 && (int64_t)splits * T * ((N + 127) / 128 * 128) > ws_cap_) --splits;
   }
