@@ -395,6 +395,18 @@ TDP_DEV void tc_mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
                  : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
 }
+#ifdef TDP_TC_PROF
+// measurement build only: cycles per wait site summed over lane 0 of every warp
+__device__ unsigned long long g_tc_prof[16];
+#define TC_PW(k, call)                      \
+  do {                                      \
+    const long long t0_ = clock64();        \
+    call;                                   \
+    prof[k] += clock64() - t0_;             \
+  } while (0)
+#else
+#define TC_PW(k, call) call
+#endif
 TDP_DEV void tc_mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -575,6 +587,10 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   }
   __syncthreads();
   const int n_items = pfx[p.n] * p.Hkv;
+#ifdef TDP_TC_PROF
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long prof_t0 = clock64();
+#endif
   // Every K / V page, the newest token's included, and q were written by
   // earlier kernels; nothing is read before the wait.
   pdl_wait();
@@ -612,7 +628,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     for (int n = 0;; ++n) {
       const int idx = cur;
       const int q = n % Q;
-      if (n >= Q) tc_mbar_wait(&iempty[q], ((uint32_t)(n / Q) & 1u) ^ 1u);
+      if (n >= Q) TC_PW(0, tc_mbar_wait(&iempty[q], ((uint32_t)(n / Q) & 1u) ^ 1u));
       int pend = 0;
       if (lane == 0) {
         s_item[q] = idx;
@@ -633,15 +649,20 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           int& cw = w == 0 ? c0 : w == 1 ? c1 : w == 2 ? c2 : c3;
           const int s = w + NWC * (cw % RW), use = cw / RW;
           ++cw;
-          if (use > 0) tc_mbar_wait(&empty[s], ((uint32_t)use & 1u) ^ 1u);
-          if (lane == 0) {
+          if (use > 0) TC_PW(1, tc_mbar_wait(&empty[s], ((uint32_t)use & 1u) ^ 1u));
+          // the page's 2 x NB TMA boxes (K halves, then V halves) are issued by
+          // 2 x NB lanes at once: the producer warp's issue rate, not the ring,
+          // limited the stream (profiling build TDP_TC_PROF: the producer waited for
+          // a free slot only 8-10 % of its time while the consumers waited for
+          // pages 56-73 %; profiles/r2/ab/tc_attn_*)
+          {
             const int row = ((blk * 2) * p.Hkv + it.kh) * kBlock;
             uint8_t* dst = ring + s * SLOT;
-            tc_mbar_expect(&full[s], SLOT);
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              tma_load_3d_ef(dst + b * 2048, &kvmap, b * 64, row, p.layer, &full[s], pol);
-              tma_load_3d_ef(dst + PAGE + b * 2048, &kvmap, b * 64, row + p.Hkv * kBlock, p.layer, &full[s], pol);
+            if (lane == 0) tc_mbar_expect(&full[s], SLOT);
+            __syncwarp();
+            if (lane < 2 * NB) {
+              const int b = lane % NB, v = lane / NB;
+              tma_load_3d_ef(dst + v * PAGE + b * 2048, &kvmap, b * 64, row + v * p.Hkv * kBlock, p.layer, &full[s], pol);
             }
           }
         }
@@ -657,7 +678,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   } else if (warp == NWC + 1) {   // ------------------------------------------ q-prep
     for (int n = 0;; ++n) {
       const int q = n % Q;
-      tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u);
+      TC_PW(2, tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u));
       int idx = 0;
       if (lane == 0) idx = s_item[q];   // read by the lane whose qready arrival orders it
       idx = __shfl_sync(0xffffffffu, idx, 0);
@@ -679,11 +700,11 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   } else if (warp == NWC + 2) {   // ------------------------------------------ merger
     for (int n = 0;; ++n) {
       const int q = n % Q, b = n & 1;
-      tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u);
+      TC_PW(3, tc_mbar_wait(&ifull[q], (uint32_t)(n / Q) & 1u));
       const int idx = s_item[q];
       if (idx < 0) break;
       const Item it = s_desc[q];
-      tc_mbar_wait(&oready[b], (uint32_t)(n >> 1) & 1u);
+      TC_PW(4, tc_mbar_wait(&oready[b], (uint32_t)(n >> 1) & 1u));
       const float* so = obuf + b * (Lay::OBUF / 4);
       const float* sm = so + NWC * G * OS;      // [4][8]
       const float* sl = sm + NWC * 8;           // [4][8]
@@ -805,7 +826,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     int cw = 0;   // pages this warp has taken (its slots: warp, warp + 4, ...)
     for (int n = 0;; ++n) {
       const int q = n % Q, b = n & 1;
-      tc_mbar_wait(&qready[q], (uint32_t)(n / Q) & 1u);
+      TC_PW(5, tc_mbar_wait(&qready[q], (uint32_t)(n / Q) & 1u));
       const int idx = s_item[q];
       if (idx < 0) break;
       const Item it = s_desc[q];
@@ -823,7 +844,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // heads 2t4, 2t4+1
       for (int j = warp; j < it.npg; j += NWC, ++cw) {
         const int s = warp + NWC * (cw % RW);
-        tc_mbar_wait(&full[s], (uint32_t)(cw / RW) & 1u);
+        TC_PW(6, tc_mbar_wait(&full[s], (uint32_t)(cw / RW) & 1u));
         const uint32_t kt = smem_u32(ring + s * SLOT), vt = kt + PAGE;
         float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -867,7 +888,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
         l0 += __shfl_xor_sync(0xffffffffu, l0, off);
         l1 += __shfl_xor_sync(0xffffffffu, l1, off);
       }
-      if (n >= 2) tc_mbar_wait(&ofree[b], ((uint32_t)(n >> 1) & 1u) ^ 1u);
+      if (n >= 2) TC_PW(7, tc_mbar_wait(&ofree[b], ((uint32_t)(n >> 1) & 1u) ^ 1u));
       float* so = obuf + b * (Lay::OBUF / 4);
       float* sm = so + NWC * G * OS;
       float* sl = sm + NWC * 8;
@@ -890,6 +911,14 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       tc_mbar_arrive(&oready[b]);
     }
   }
+#ifdef TDP_TC_PROF
+  if (lane == 0) {
+    for (int k = 0; k < 8; ++k) atomicAdd(&g_tc_prof[k], (unsigned long long)prof[k]);
+    // 8 + role: total cycles of the warp (consumers 8, producer 9, q-prep 10, merger 11)
+    const int role = warp < NWC ? 8 : 9 + (warp - NWC);
+    atomicAdd(&g_tc_prof[role], (unsigned long long)(clock64() - prof_t0));
+  }
+#endif
   __syncthreads();
   // every producer of the grid has fetched past the end before its CTA counts
   // itself done: the last CTA re-arms the work counters for the next launch
@@ -898,6 +927,17 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
     p.work[1] = 0;
   }
 }
+
+#ifdef TDP_TC_PROF
+void tc_prof_read(unsigned long long* out, bool reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_tc_prof, sizeof(g_tc_prof));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+  }
+}
+#endif
 
 bool make_kv_map(CUtensorMap* map, const bf16* pool, int64_t C, int Hkv, int hd, int n_layers) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;

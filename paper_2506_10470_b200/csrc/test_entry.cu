@@ -405,3 +405,9 @@ namespace tdp { void chain_trace_read(unsigned long long* out); }
 // measurement builds only: the decode chain's trace buffer (see decode_chain.cu)
 extern "C" void td_chain_trace(unsigned long long* out) { tdp::chain_trace_read(out); }
 #endif
+
+#ifdef TDP_TC_PROF
+namespace tdp { void tc_prof_read(unsigned long long* out, bool reset); }
+// measurement builds only: the tensor-core decode attention's per-wait-site cycle sums
+extern "C" void td_tc_prof(unsigned long long* out, int32_t reset) { tdp::tc_prof_read(out, reset != 0); }
+#endif
