@@ -413,11 +413,12 @@ TDP_DEV void tc_mbar_arrive(uint64_t* b) {
 TDP_DEV void tc_mbar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
-TDP_DEV void tma_load_3d_ef(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar, uint64_t pol) {
+TDP_DEV void tma_load_4d_ef(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3, uint64_t* bar,
+                            uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
-      "%4}], [%5], %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 TDP_DEV void ldsm4(uint32_t* r, uint32_t addr) {
@@ -442,7 +443,13 @@ TDP_DEV void hmma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
 }
 // byte offset of (row r, 16-byte chunk ch) in a page staged as hd/64 boxes of
 // [16 rows][128 B] with the 128B swizzle (chunk ^ (row & 7))
-TDP_DEV uint32_t page_off(int r, int ch) { return (uint32_t)((ch >> 3) * 2048 + r * 128 + (((ch & 7) ^ (r & 7)) << 4)); }
+// a page staged by ONE 4-D box (64 columns x hd/64 halves x 16 rows): 128-B row
+// segments ordered (row, half), 128B swizzle on the segment index
+template <int NB>
+TDP_DEV uint32_t page_off(int r, int ch) {
+  const int seg = r * NB + (ch >> 3);
+  return (uint32_t)(seg * 128 + (((ch & 7) ^ (seg & 7)) << 4));
+}
 }  // namespace
 
 constexpr int kTcRing = 8;          // page ring slots (a multiple of the 4 consumer warps)
@@ -650,8 +657,9 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           const int s = w + NWC * (cw % RW), use = cw / RW;
           ++cw;
           if (use > 0) TC_PW(1, tc_mbar_wait(&empty[s], ((uint32_t)use & 1u) ^ 1u));
-          // the page's 2 x NB TMA boxes (K halves, then V halves) are issued by
-          // 2 x NB lanes at once: the producer warp's issue rate, not the ring,
+          // the page's K and V boxes are issued by 2 lanes at once, one 4-D box
+          // each (not 2 x NB 64-column boxes from lane 0): the producer warp's
+          // issue rate, not the ring,
           // limited the stream (profiling build TDP_TC_PROF: the producer waited for
           // a free slot only 8-10 % of its time while the consumers waited for
           // pages 56-73 %; profiles/r2/ab/tc_attn_*)
@@ -660,10 +668,8 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
             uint8_t* dst = ring + s * SLOT;
             if (lane == 0) tc_mbar_expect(&full[s], SLOT);
             __syncwarp();
-            if (lane < 2 * NB) {
-              const int b = lane % NB, v = lane / NB;
-              tma_load_3d_ef(dst + v * PAGE + b * 2048, &kvmap, b * 64, row + v * p.Hkv * kBlock, p.layer, &full[s], pol);
-            }
+            if (lane < 2)   // K, V: one 4-D box each (both 64-column halves)
+              tma_load_4d_ef(dst + lane * PAGE, &kvmap, 0, 0, row + lane * p.Hkv * kBlock, p.layer, &full[s], pol);
           }
         }
       }
@@ -850,7 +856,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
 #pragma unroll
         for (int jj = 0; jj < KS; ++jj) {
           uint32_t a[4];
-          ldsm4(a, kt + page_off(k_row, 2 * jj + k_ch));
+          ldsm4(a, kt + page_off<NB>(k_row, 2 * jj + k_ch));
           hmma16816(sc, a, qb[jj][0], qb[jj][1]);
         }
         const int tb = (it.pg0 + j) << 4;
@@ -878,7 +884,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           o[d][2] *= c0;
           o[d][3] *= c1;
           uint32_t a[4];
-          ldsm4_t(a, vt + page_off(v_row, 2 * d + v_ch));
+          ldsm4_t(a, vt + page_off<NB>(v_row, 2 * d + v_ch));
           hmma16816(o[d], a, b0, b1);
         }
         tc_mbar_arrive(&empty[s]);   // this thread is done with the slot
@@ -951,11 +957,12 @@ bool make_kv_map(CUtensorMap* map, const bf16* pool, int64_t C, int Hkv, int hd,
   }
   if (hd < 64 || hd % 64) return false;
   const int64_t rows = C * 2 * Hkv * kBlock;
-  cuuint64_t dims[3] = {(cuuint64_t)hd, (cuuint64_t)rows, (cuuint64_t)std::max(n_layers, 1)};
-  cuuint64_t strides[2] = {(cuuint64_t)hd * 2, (cuuint64_t)(rows * hd * 2)};
-  cuuint32_t box[3] = {64, (cuuint32_t)kBlock, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<bf16*>(pool), dims, strides, box, estr,
+  // (64 columns, hd/64 halves, page rows, layers): one box = a whole 16-token page
+  cuuint64_t dims[4] = {64, (cuuint64_t)(hd / 64), (cuuint64_t)rows, (cuuint64_t)std::max(n_layers, 1)};
+  cuuint64_t strides[3] = {128, (cuuint64_t)hd * 2, (cuuint64_t)(rows * hd * 2)};
+  cuuint32_t box[4] = {64, (cuuint32_t)(hd / 64), (cuuint32_t)kBlock, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<bf16*>(pool), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -155,9 +155,9 @@ struct DecodeAttnParams {
   const int32_t* order = nullptr;   // [n] sequences longest-first for the tensor-core kernel's items (nullable)
   int impl = 0;          // 0: kernel by shape (tensor cores for GQA hd 64/128); 1: SIMT; 2: tensor cores (td_bench_attn)
 };
-// 3-D TMA descriptor of a KV pool [n_layers][C blocks][K|V][Hkv][16][hd] bf16
-// viewed as (hd, C*2*Hkv*16 page rows, n_layers), box (64, 16, 1), 128B
-// swizzle: one box = half (hd 128) or all (hd 64) of a 16-token K or V page.
+// 4-D TMA descriptor of a KV pool [n_layers][C blocks][K|V][Hkv][16][hd] bf16
+// viewed as (64 columns, hd/64 halves, C*2*Hkv*16 page rows, n_layers), box
+// (64, hd/64, 16, 1), 128B swizzle: one box = a whole 16-token K or V page.
 bool make_kv_map(CUtensorMap* map, const bf16* pool, int64_t C, int Hkv, int hd, int n_layers);
 void launch_decode_attn(const DecodeAttnParams& p, cudaStream_t st);
 // Launch plan from the host copy of the context lengths: sets split_tokens
