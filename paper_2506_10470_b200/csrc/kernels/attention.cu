@@ -398,14 +398,14 @@ TDP_DEV void tc_mbar_wait(uint64_t* b, uint32_t parity) {
 #ifdef TDP_TC_PROF
 // measurement build only: cycles per wait site summed over lane 0 of every warp
 __device__ unsigned long long g_tc_prof[16];
-#define TC_PW(k, call)                      \
+#define TC_PW(k, ...)                       \
   do {                                      \
     const long long t0_ = clock64();        \
-    call;                                   \
+    __VA_ARGS__;                            \
     prof[k] += clock64() - t0_;             \
   } while (0)
 #else
-#define TC_PW(k, call) call
+#define TC_PW(k, ...) __VA_ARGS__
 #endif
 TDP_DEV void tc_mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -451,6 +451,35 @@ TDP_DEV uint32_t page_off(int r, int ch) {
   return (uint32_t)(seg * 128 + (((ch & 7) ^ (seg & 7)) << 4));
 }
 }  // namespace
+
+// n contiguous floats from shared memory (16-byte aligned for n % 4 == 0, else 8)
+template <int N>
+TDP_DEV void ld_vec(float (&v)[N], const float* src) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+      const float4 t = *reinterpret_cast<const float4*>(src + i);
+      v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const float2 t = *reinterpret_cast<const float2*>(src + i);
+      v[i] = t.x; v[i + 1] = t.y;
+    }
+  }
+}
+// n floats -> n contiguous bf16 (round to nearest), one store of 2n bytes
+template <int N>
+TDP_DEV void st_bf16_vec(bf16* dst, const float (&r)[N]) {
+  if constexpr (N == 2) {
+    *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(r[0], r[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; i += 4)
+      *reinterpret_cast<uint2*>(dst + i) = make_uint2(pack_bf16x2(r[i], r[i + 1]), pack_bf16x2(r[i + 2], r[i + 3]));
+  }
+}
 
 constexpr int kTcRing = 8;          // page ring slots (a multiple of the 4 consumer warps)
 constexpr int kTcItemQ = 3;         // work items in flight per CTA (queue slots)
@@ -500,6 +529,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   constexpr int KS = HD / 16;                    // k-steps of S^T / m-tiles of O^T
   constexpr int OS = HD + kTcPad;                // sO row stride (floats)
   constexpr int RW = R / 4;                      // ring slots per consumer warp
+  constexpr int CPL = HD / 32;                   // merger: output columns per lane
   static_assert(G >= 1 && G <= 8 && R % NWC == 0, "layout");
   extern __shared__ uint8_t tc_smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
@@ -595,7 +625,7 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   __syncthreads();
   const int n_items = pfx[p.n] * p.Hkv;
 #ifdef TDP_TC_PROF
-  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof[16] = {};
   const long long prof_t0 = clock64();
 #endif
   // Every K / V page, the newest token's included, and q were written by
@@ -663,23 +693,25 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           // limited the stream (profiling build TDP_TC_PROF: the producer waited for
           // a free slot only 8-10 % of its time while the consumers waited for
           // pages 56-73 %; profiles/r2/ab/tc_attn_*)
-          {
+          TC_PW(12, {
             const int row = ((blk * 2) * p.Hkv + it.kh) * kBlock;
             uint8_t* dst = ring + s * SLOT;
             if (lane == 0) tc_mbar_expect(&full[s], SLOT);
             __syncwarp();
             if (lane < 2)   // K, V: one 4-D box each (both 64-column halves)
               tma_load_4d_ef(dst + lane * PAGE, &kvmap, 0, 0, row + lane * p.Hkv * kBlock, p.layer, &full[s], pol);
-          }
+          });
         }
       }
       // rotate: the next item was fetched (and its table chunk loaded) one item ago
-      const int after = nxt >= 0 ? __shfl_sync(0xffffffffu, pend, 0) : -1;
-      cur = nxt;
-      it_cur = it_nxt;
-      bt_cur = bt_nxt;
-      nxt = after >= 0 && after < n_items ? after : -1;
-      bt_nxt = chunk0(nxt, it_nxt);
+      TC_PW(13, {
+        const int after = nxt >= 0 ? __shfl_sync(0xffffffffu, pend, 0) : -1;
+        cur = nxt;
+        it_cur = it_nxt;
+        bt_cur = bt_nxt;
+        nxt = after >= 0 && after < n_items ? after : -1;
+        bt_nxt = chunk0(nxt, it_nxt);
+      });
     }
   } else if (warp == NWC + 1) {   // ------------------------------------------ q-prep
     for (int n = 0;; ++n) {
@@ -714,7 +746,13 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       const float* so = obuf + b * (Lay::OBUF / 4);
       const float* sm = so + NWC * G * OS;      // [4][8]
       const float* sl = sm + NWC * 8;           // [4][8]
-      float A[G][HD / 32], Mg[G], Lg[G];
+      // lane owns the CPL contiguous columns [lane CPL, lane CPL + CPL): vector
+      // shared loads and one packed global store per head (the strided 2-byte
+      // stores took 75-78 % of this warp at contexts 128-256; TDP_TC_PROF)
+      float A[G][CPL], Mg[G], Lg[G];
+#ifdef TDP_TC_PROF
+      const long long tm0_ = clock64();
+#endif
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float M = -INFINITY;
@@ -727,11 +765,13 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           L += sl[w * 8 + g] * c[w];
         }
 #pragma unroll
-        for (int dd = 0; dd < HD / 32; ++dd) {
-          float a = 0.f;
+        for (int dd = 0; dd < CPL; ++dd) A[g][dd] = 0.f;
 #pragma unroll
-          for (int w = 0; w < NWC; ++w) a += so[(w * G + g) * OS + dd * 32 + lane] * c[w];
-          A[g][dd] = a;
+        for (int w = 0; w < NWC; ++w) {
+          float v[CPL];
+          ld_vec<CPL>(v, so + (w * G + g) * OS + lane * CPL);
+#pragma unroll
+          for (int dd = 0; dd < CPL; ++dd) A[g][dd] += v[dd] * c[w];
         }
         Mg[g] = M;
         Lg[g] = L;
@@ -739,23 +779,31 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
       const Item itc = it;
       tc_mbar_arrive(&ofree[b]);    // the consumers may reuse result buffer b
       tc_mbar_arrive(&iempty[q]);   // queue slot q (descriptor, q buffer) free: the results are in registers
+#ifdef TDP_TC_PROF
+      const long long tm1_ = clock64();
+      prof[14] += tm1_ - tm0_;
+#endif
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int h = itc.kh * G + g;
         if (itc.n_splits == 1) {
+          // one reciprocal per head (as the split merge): no per-element
+          // division, whose slow path a zero numerator takes
+          const float inv = 1.f / Lg[g];
+          float r[CPL];
 #pragma unroll
-          for (int dd = 0; dd < HD / 32; ++dd)
-            p.o[((int64_t)itc.seq * H + h) * HD + dd * 32 + lane] = __float2bfloat16_rn(A[g][dd] / Lg[g]);
+          for (int dd = 0; dd < CPL; ++dd) r[dd] = A[g][dd] * inv;
+          st_bf16_vec<CPL>(p.o + ((int64_t)itc.seq * H + h) * HD + lane * CPL, r);
         } else {
           float* part = p.part + (((int64_t)itc.seq * H + h) * p.max_splits + itc.split) * (HD + 2);
 #pragma unroll
-          for (int dd = 0; dd < HD / 32; ++dd) __stcg(part + 2 + dd * 32 + lane, A[g][dd]);
-          if (lane == 0) {
-            __stcg(part, Mg[g]);
-            __stcg(part + 1, Lg[g]);
-          }
+          for (int dd = 0; dd < CPL; dd += 2) __stcg(reinterpret_cast<float2*>(part + 2 + lane * CPL + dd), make_float2(A[g][dd], A[g][dd + 1]));
+          if (lane == 0) __stcg(reinterpret_cast<float2*>(part), make_float2(Mg[g], Lg[g]));
         }
       }
+#ifdef TDP_TC_PROF
+      prof[15] += clock64() - tm1_;
+#endif
       if (itc.n_splits > 1) {
         __syncwarp();
         int last = 0;
@@ -771,9 +819,9 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
           // (m, l) of every (head, split) in one round trip, staged in shared memory
           for (int e = lane; e < G * ns; e += 32) {
             const int g = e / ns, s2 = e - g * ns;
-            const float* ps = part0 + ((int64_t)g * p.max_splits + s2) * (HD + 2);
-            s_c[g][s2] = __ldcg(ps);
-            s_l[g][s2] = __ldcg(ps + 1);
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(part0 + ((int64_t)g * p.max_splits + s2) * (HD + 2)));
+            s_c[g][s2] = ml.x;
+            s_l[g][s2] = ml.y;
           }
           __syncwarp();
           float Lh[G];
@@ -788,36 +836,41 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
             for (int s2 = lane; s2 < ns; s2 += 32) s_c[g][s2] = exp2f(s_c[g][s2] - M);
             __syncwarp();
           }
-          float acc[G][HD / 32];
+          float acc[G][CPL];
 #pragma unroll
           for (int g = 0; g < G; ++g)
 #pragma unroll
-            for (int dd = 0; dd < HD / 32; ++dd) acc[g][dd] = 0.f;
-          for (int s2 = 0; s2 < ns; s2 += 2) {   // split order; 2 splits x G x HD/32 loads in flight
-            float v0[G][HD / 32], v1[G][HD / 32];
+            for (int dd = 0; dd < CPL; ++dd) acc[g][dd] = 0.f;
+          for (int s2 = 0; s2 < ns; s2 += 2) {   // split order; 2 splits x G x CPL values in flight
+            float v0[G][CPL], v1[G][CPL];
             const bool two = s2 + 1 < ns;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-              const float* ps = part0 + ((int64_t)g * p.max_splits + s2) * (HD + 2) + 2;
+              const float* ps = part0 + ((int64_t)g * p.max_splits + s2) * (HD + 2) + 2 + lane * CPL;
 #pragma unroll
-              for (int dd = 0; dd < HD / 32; ++dd) {
-                v0[g][dd] = __ldcg(ps + dd * 32 + lane);
-                v1[g][dd] = two ? __ldcg(ps + (HD + 2) + dd * 32 + lane) : 0.f;
+              for (int dd = 0; dd < CPL; dd += 2) {
+                const float2 a0 = __ldcg(reinterpret_cast<const float2*>(ps + dd));
+                const float2 a1 = two ? __ldcg(reinterpret_cast<const float2*>(ps + (HD + 2) + dd)) : make_float2(0.f, 0.f);
+                v0[g][dd] = a0.x;
+                v0[g][dd + 1] = a0.y;
+                v1[g][dd] = a1.x;
+                v1[g][dd + 1] = a1.y;
               }
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               const float c0 = s_c[g][s2], c1 = two ? s_c[g][s2 + 1] : 0.f;
 #pragma unroll
-              for (int dd = 0; dd < HD / 32; ++dd) acc[g][dd] = acc[g][dd] + c0 * v0[g][dd] + c1 * v1[g][dd];
+              for (int dd = 0; dd < CPL; ++dd) acc[g][dd] = acc[g][dd] + c0 * v0[g][dd] + c1 * v1[g][dd];
             }
           }
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const float inv = 1.f / Lh[g];
+            float r[CPL];
 #pragma unroll
-            for (int dd = 0; dd < HD / 32; ++dd)
-              p.o[((int64_t)itc.seq * H + itc.kh * G + g) * HD + dd * 32 + lane] = __float2bfloat16_rn(acc[g][dd] * inv);
+            for (int dd = 0; dd < CPL; ++dd) r[dd] = acc[g][dd] * inv;
+            st_bf16_vec<CPL>(p.o + ((int64_t)itc.seq * H + itc.kh * G + g) * HD + lane * CPL, r);
           }
           __syncwarp();
           if (lane == 0) p.counters[itc.seq * p.Hkv + itc.kh] = 0;
@@ -919,7 +972,8 @@ decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, DecodeAttnParam
   }
 #ifdef TDP_TC_PROF
   if (lane == 0) {
-    for (int k = 0; k < 8; ++k) atomicAdd(&g_tc_prof[k], (unsigned long long)prof[k]);
+    for (int k = 0; k < 16; ++k)
+      if (k < 8 || k >= 12) atomicAdd(&g_tc_prof[k], (unsigned long long)prof[k]);
     // 8 + role: total cycles of the warp (consumers 8, producer 9, q-prep 10, merger 11)
     const int role = warp < NWC ? 8 : 9 + (warp - NWC);
     atomicAdd(&g_tc_prof[role], (unsigned long long)(clock64() - prof_t0));

@@ -164,6 +164,20 @@ extern "C" td_status td_test_gemm(int32_t device, const uint16_t* A, const uint1
   return st;
 }
 
+// Benchmark operands: seeded uniform [-1, 1] bf16 (the weight-init hash), not
+// zeros -- an all-zero KV pool sends every attention output 0 / l down the
+// division slow path and zero operands draw less power than real data.
+static void fill_uniform(bf16* dst, int64_t elems, uint64_t seed, cudaStream_t st) {
+  const int cols = 64;
+  InitSpec sp{};
+  sp.map = kMapIdentity;
+  sp.kind = kInitEmbed;
+  sp.rows = (int)(elems / cols);
+  sp.cols = cols;
+  sp.tid0 = (int)(seed & 0xffff);
+  if (sp.rows > 0) launch_init(dst, sp, seed, st);
+}
+
 extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t K, int32_t splits, int32_t decode,
                                    int32_t iters, int32_t copies, float* us_per_call) {
   if (T < 1 || N < 2 || (N & 1) || K < 64 || K % 64 || iters < 1 || copies < 1 || !us_per_call) return TD_EINVAL;
@@ -184,8 +198,8 @@ extern "C" td_status td_bench_gemm(int32_t device, int32_t T, int32_t N, int32_t
       cudaMalloc(&cnt, 65536 * 4)) {
     st = TD_ENOMEM;
   } else {
-    for (auto& w : Ws) cudaMemset(w, 0, (size_t)Np * K * 2);
-    cudaMemset(dA, 0, (size_t)Tcap * K * 2);
+    for (size_t i = 0; i < Ws.size(); ++i) fill_uniform(Ws[i], (int64_t)Np * K, 11 + i, s);
+    fill_uniform(dA, (int64_t)Tcap * K, 7, s);
     cudaMemset(cnt, 0, 65536 * 4);
     EpiParams ep{};
     ep.mode = kEpiF32;
@@ -277,8 +291,8 @@ extern "C" td_status td_bench_attn(int32_t device, int32_t n, const int32_t* ctx
       cudaMalloc(&cnt, ((size_t)n * Hkv + 2) * 4)) {
     st = TD_ENOMEM;
   } else {
-    cudaMemset(kv, 0, pool * blk_bytes);
-    cudaMemset(q, 0, (size_t)n * H * hd * 2);
+    fill_uniform(kv, (int64_t)(pool * blk_bytes / 2), 5, s);
+    fill_uniform(q, (int64_t)n * H * hd, 6, s);
     cudaMemset(cnt, 0, ((size_t)n * Hkv + 2) * 4);
     cudaMemcpy(dctx, ctx, n * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice);

@@ -18,8 +18,9 @@ fn.argtypes = [C.c_void_p, C.c_int32]
 fn.restype = None
 buf = np.zeros(16, np.uint64)
 NAMES = ["prod.wait_iempty", "prod.wait_ring_slot", "qprep.wait_ifull", "merger.wait_ifull", "merger.wait_oready",
-         "cons.wait_qready", "cons.wait_page", "cons.wait_ofree"]
-for n, ctx in ((512, 256), (512, 1024), (64, 314), (256, 314)):
+         "cons.wait_qready", "cons.wait_page", "cons.wait_ofree", None, None, None, None,
+         "prod.page_issue", "prod.rotate", "merger.combine", "merger.store"]
+for n, ctx in ((512, 256), (512, 1024), (64, 314), (256, 314), (512, 128)):
     c = np.full(n, ctx, np.int32)
     td_bench_attn(c, 64, 8, 128, iters=2)
     fn(buf.ctypes.data, 1)
@@ -29,6 +30,8 @@ for n, ctx in ((512, 256), (512, 1024), (64, 314), (256, 314)):
     row = {"n": n, "ctx": ctx, "us": round(us, 2),
            "frac": round(float(c.sum()) * 8 * 128 * 4 / (us * 1e-6) / 1e9 / 6551.7, 3)}
     for i, k in enumerate(NAMES):
+        if k is None:
+            continue
         role = k.split(".")[0]
         row[k] = round(float(buf[i]) / max(float(tot[role]), 1.0), 3)
     print(json.dumps(row), flush=True)
