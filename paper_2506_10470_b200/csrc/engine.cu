@@ -453,7 +453,7 @@ td_status CudaEngine::init(const td_model_shape& s, int n_stages, const td_optio
   if (C_ < 1) { error = "no room for the KV pool"; return TD_ENOMEM; }
   if (cudaMalloc(&kv_, C_ * per_block) != cudaSuccess) { error = "KV pool allocation failed"; return TD_ENOMEM; }
   CK(cudaMemsetAsync(kv_, 0, C_ * per_block, st_));
-  if (hd_ >= 64 && H_ != Hkv_) {
+  if (hd_ >= 64) {   // GQA always, MHA for large long-context decode batches (decode_attn_use_tc)
     have_kvmap_ = make_kv_map(&kvmap_, kv_, C_, Hkv_, hd_, own_l1_ - own_l0_);
     if (!have_kvmap_) { error = "cuTensorMapEncodeTiled failed (KV pool)"; return TD_ECUDA; }
   }
@@ -792,6 +792,9 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
   const int nqkv = (H_ + 2 * Hkv_) * hd_;
   const float eps = s_.rms_eps;
   const bool dec = !M.prefill;
+  // pure decode on the tensor-core attention kernel (GQA; MHA at large batches
+  // of long contexts): the QKV split-K reduction then runs as its own kernel
+  const bool attn_tc = dec && !M.hybrid && have_kvmap_ && decode_attn_use_tc(n, H_, Hkv_, hd_, mb_ctx_.data());
   bool normed = false;   // a_ already holds RMSNorm(x; g1) (fused into the embedding / the previous down-proj reduction)
   if (stage == 0) {   // + the first layer's input norm
     launch_embed(arena, dm + M.o_tokidx, E_, x_, T, d_, st_, L_[stage_l0_[stage]].g1, a_, eps);
@@ -824,7 +827,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
     // (not for the tensor-core GQA kernel: its single q-prep warp would redo
     // the reduction for every split item of a sequence; the split-K reduce
     // kernel does it once per token and the kernel bulk-copies q)
-    const bool defer_qkv = dec && !M.hybrid && !(have_kvmap_ && Hkv_ < H_);
+    const bool defer_qkv = dec && !M.hybrid && !attn_tc;
     const int qsplits = gemm(xa_, w.tqkv, T, nqkv, d_, ep, dec, /*defer=*/defer_qkv);
     tend(iq, (double)nqkv * d_ * 2 + (double)T * d_ * 2 + (double)T * nqkv * 2, 2.0 * T * nqkv * d_);
     if (M.hybrid) {
@@ -868,6 +871,7 @@ td_status CudaEngine::run_stage(int stage, const Meta& M, const int32_t* dm, int
       dp.layer = l - own_l0_;
       dp.work = attn_cnt_ + capN_ * Hkv_;
       dp.order = dm + M.o_ord;
+      dp.impl = attn_tc ? 2 : 1;
       if (defer_qkv && qsplits > 1) {
         dp.qkv_ws = ws_;
         dp.qkv_splits = qsplits;

@@ -1048,6 +1048,22 @@ static bool use_tc(const DecodeAttnParams& p) {
   return G >= 2 || p.impl == 2;
 }
 
+bool decode_attn_use_tc(int n, int H, int Hkv, int hd, const int* ctx) {
+  if ((hd != 64 && hd != 128) || Hkv < 1 || H / Hkv > 8) return false;
+  if (H > Hkv) return true;
+#ifdef TDP_NO_MHA_TC
+  return false;
+#else
+  if (n < kMhaTcMinN) return false;
+#ifndef TDP_MHA_TC_V1
+  if (n < kMhaTcMaxN) return true;
+#endif
+  int64_t sum = 0;
+  for (int i = 0; i < n; ++i) sum += ctx[i];
+  return sum >= (int64_t)kMhaTcMinMeanCtx * n;
+#endif
+}
+
 template <int HD>
 static void launch_decode_hd(const DecodeAttnParams& p, cudaStream_t st) {
   const int G = p.H / p.Hkv;

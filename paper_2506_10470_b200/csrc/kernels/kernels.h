@@ -175,6 +175,18 @@ constexpr int kAttnMinSplitGQA = 32;
 constexpr int kAttnPdlMaxN = TDP_ATTN_PDL_MAXN;   // decode attention as a PDL dependent up to this batch size
 constexpr int kAttnSmallN = 32;
 void plan_decode_attn(DecodeAttnParams& p, const int* ctx_host);
+// Which decode-attention kernel a pure decode micro-batch should use (the
+// engine decides before the QKV GEMM: the SIMT kernel can absorb the QKV
+// split-K reduction, the tensor-core one cannot).  GQA (hd 64 / 128, G <= 8):
+// tensor cores.  MHA: tensor cores for kMhaTcMinN <= n < kMhaTcMaxN sequences
+// (mixed lengths: its dynamic item queue balances them, 0.78 / 0.87 vs SIMT
+// 0.65 / 0.81 of HBM at n = 64 / 128, mean context 250), and above that at a
+// mean context >= kMhaTcMinMeanCtx tokens; else SIMT (random-data sweep,
+// profiles/r2/attn_sweep_mha_random.jsonl).
+constexpr int kMhaTcMinN = 64;
+constexpr int kMhaTcMaxN = 256;
+constexpr int kMhaTcMinMeanCtx = 512;
+bool decode_attn_use_tc(int n, int H, int Hkv, int hd, const int* ctx_host);
 
 // Prefill: varlen causal over each sequence's own (paged) K/V.
 struct PrefillAttnParams {

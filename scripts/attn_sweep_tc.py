@@ -19,9 +19,11 @@ impls = [int(a) for a in sys.argv[4:]] or [0]
 splits = [int(s) for s in os.environ.get("SPLITS", "0,64,128,256,512,1024").split(",")]
 rng = np.random.default_rng(0)
 for n in (1, 4, 16, 64, 128, 256, 512):
-    for dist in ("256", "1024", "3072", "mix"):
+    for dist in ("256", "1024", "3072", "mix", "mix250"):
         if dist == "mix":
             ctx = np.clip(rng.lognormal(6.3, 0.8, n), 32, 4000).astype(np.int32)
+        elif dist == "mix250":   # C2-like decode contexts (mean ~250 tokens)
+            ctx = np.clip(rng.lognormal(5.2, 0.8, n), 16, 2000).astype(np.int32)
         else:
             ctx = np.full(n, int(dist), np.int32)
         kv_bytes = float(ctx.sum()) * HKV * HD * 2 * 2 + 4.0 * n * H * HD

@@ -418,6 +418,37 @@ def test_device_weights_bit_identical_to_oracle_recipe():
         assert Wt.tensor_id(0, "lm", L) == 2 + 9 * L
 
 
+@pytest.mark.slow
+def test_mha_tensor_core_decode_large_batch():
+    """MHA decode micro-batches of >= 64 sequences at a mean context >= 512
+    tokens run on the tensor-core attention kernel (decode_attn_use_tc), with
+    the QKV split-K reduction as its own kernel: sampled sequences vs the fp64
+    oracle, and the same sequences decoded in an 8-sequence micro-batch (SIMT
+    kernel, reduction folded into it) agree within the tolerance."""
+    shape = ModelShape("mha128", 1, 512, 4, 4, 512, 512, max_seq_len=4096)
+    W = OracleWeights(shape)
+    rng = np.random.default_rng(17)
+    n = 72
+    lengths = [int(v) for v in rng.integers(300, 1200, size=n)]
+    assert sum(lengths) >= 512 * n
+    prompts = [rng.integers(0, shape.vocab, size=L).astype(np.int32) for L in lengths]
+    t = TDPipe(shape, 1, kv_blocks=sum((L + 2 + 15) // 16 + 1 for L in lengths) + 8)   # _paged leaves a gap per sequence
+    bt = _paged([L + 2 for L in lengths])
+    out = _prefill_in_budget(t, prompts, bt)
+    nxt = np.argmax(out, -1).astype(np.int32)
+    out2 = t.td_stage_forward(0, TD_BATCH_DECODE, lengths, [1] * n, bt, nxt)
+    out_small = t.td_stage_forward(0, TD_BATCH_DECODE, lengths[:8], [1] * 8, bt[:8], nxt[:8])
+    t.close()
+    order = sorted(range(n), key=lambda i: lengths[i])
+    idx = sorted(set(order[:2] + order[-2:] + [int(i) for i in rng.choice(n, 3, replace=False)]))
+    for i in idx:
+        ref = F.sequence_logits(W, np.concatenate([prompts[i], [nxt[i]]]))
+        _rows_ok(out[i], ref[-2])
+        _rows_ok(out2[i], ref[-1])
+    for i in range(8):
+        assert F.max_abs_rel(out2[i], out_small[i]).max() <= TOL
+
+
 def test_decode_attention_long_context_many_pages():
     """Long contexts (many KV pages per split, every ring slot reused several
     times) for MHA hd=128 and GQA: decode logits vs the oracle."""
